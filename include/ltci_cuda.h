@@ -1,0 +1,211 @@
+/*
+ * ltci_cuda.h -- C-ABI of the B200 dual-scale cascade (DS-GRFT / DS-KT-MFP).
+ *
+ * This is the drop-in boundary under the reference's C++ detector API.  Every
+ * signature uses plain pointers, sizes and POD structs; no C++ or torch types.
+ * A caller holding the reference types (`ltci::FreqPulseCube`,
+ * `ltci::DualScaleSpace`, `ltci::DetectorOptions`, `ltci::DetectionMap`) fills
+ * the POD mirrors below field by field; `paper_2403_06788_b200/csrc/dropin.cpp`
+ * is that caller for C++ and `paper_2403_06788_b200/_lib.py` for Python.
+ *
+ * Reference interfaces replaced (paths relative to the reference repo root):
+ *   ltci_cuda_ds_grft      -> ltci::ds_grft    proj/include/ltci/detectors.hpp:42-43
+ *                                               proj/src/detectors.cpp:414-449
+ *   ltci_cuda_ds_kt_mfp    -> ltci::ds_kt_mfp  proj/include/ltci/detectors.hpp:47-48
+ *                                               proj/src/detectors.cpp:451-481
+ *   ltci_cuda_keystone     -> ltci::keystone   proj/include/ltci/transforms.hpp:40
+ *   ltci_cuda_mgift        -> ltci::mgift      proj/include/ltci/transforms.hpp:52-53
+ *   ltci_cuda_gft          -> ltci::gft        proj/include/ltci/transforms.hpp:74-75
+ *   ltci_cuda_detection_threshold -> ltci::detection_threshold
+ *                                               proj/include/ltci/detectors.hpp:55
+ * POD mirrors:
+ *   ltci_radar        <- RadarParams     proj/include/ltci/radar_params.hpp:15-54
+ *   ltci_grid         <- Grid            proj/include/ltci/search_space.hpp:12-22
+ *   ltci_dual_space   <- DualScaleSpace  proj/include/ltci/search_space.hpp:68-77
+ *                        (+ StepSizes :38-45, RangeRoi :30-36)
+ *   ltci_ambiguity    <- AmbiguitySpace  proj/include/ltci/search_space.hpp:84-90
+ *   ltci_options      <- DetectorOptions proj/include/ltci/detectors.hpp:14-20
+ *   ltci_detection_map<- DetectionMap    proj/include/ltci/detection.hpp:47-73
+ *
+ * Cubes cross the boundary as interleaved (re, im) float64 arrays in the
+ * reference's column-major layout, sample (k, m) at element k + K*m
+ * (proj/include/ltci/cube.hpp:10-11).  Status codes map onto the reference's
+ * exception types (see LTCI_* below); the message is in ltci_cuda_last_error().
+ */
+#ifndef LTCI_CUDA_H_
+#define LTCI_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTCI_MAX_ORDER 4
+#define LTCI_MAX_AXES 8
+
+/* status codes: the C++ shim rethrows the matching exception type */
+enum {
+    LTCI_OK = 0,
+    LTCI_INVALID_ARGUMENT = 1, /* std::invalid_argument            */
+    LTCI_CONDITION_VIOLATED = 2, /* ltci::ConditionViolated        */
+    LTCI_RUNTIME_ERROR = 3,    /* std::runtime_error (CUDA failure) */
+    LTCI_BAD_ALLOC = 4,        /* std::bad_alloc (result too large) */
+    LTCI_NO_DEVICE = 5         /* no CUDA device / extension missing */
+};
+
+/* detector kinds, same order as ltci::DetectorKind (detection.hpp:12) */
+enum { LTCI_FD_GRFT = 0, LTCI_TD_GRFT = 1, LTCI_KT_MFP = 2, LTCI_DS_GRFT = 3, LTCI_DS_KT_MFP = 4 };
+
+/* axis roles, same order as ltci::AxisDesc::Role (detection.hpp:37) */
+enum {
+    LTCI_AXIS_RANGE = 0,
+    LTCI_AXIS_VELOCITY = 1,
+    LTCI_AXIS_HIGHER = 2,
+    LTCI_AXIS_DOPPLER = 3,
+    LTCI_AXIS_COARSE = 4,
+    LTCI_AXIS_FINE = 5,
+    LTCI_AXIS_FOLDING = 6
+};
+
+/* compensation variants, ltci::DetectorVariant (transforms.hpp:11) */
+enum { LTCI_VARIANT_GRFT = 0, LTCI_VARIANT_KTMFP = 1 };
+
+/* fine-stage formulations (both compute the same sums) */
+enum {
+    LTCI_FINE_AUTO = 0,
+    LTCI_FINE_FFT_CUDA_CORE = 1, /* chirp recurrence + register/smem FFT, FP32   */
+    LTCI_FINE_TC_DENSE = 2       /* tcgen05 dense complex contraction, fp16 split */
+};
+
+typedef struct {
+    double fc, fs, Br, delta_f, PRF;
+    int32_t M, K, K_valid;
+} ltci_radar;
+
+typedef struct {
+    double start, step;
+    int32_t count;
+} ltci_grid;
+
+typedef struct {
+    ltci_radar radar;
+    int32_t order; /* P */
+    ltci_grid coarse[LTCI_MAX_ORDER]; /* index p-1 for p = 1..P */
+    ltci_grid fine[LTCI_MAX_ORDER];   /* index p-1, centred on 0, unscaled */
+    double rm_step[LTCI_MAX_ORDER];   /* StepSizes::rm  */
+    double dfm_step[LTCI_MAX_ORDER];  /* StepSizes::dfm */
+    double alpha[LTCI_MAX_ORDER];     /* StepSizes::alpha */
+    double kappa;
+    int32_t roi_first, roi_last;      /* RangeRoi, inclusive */
+} ltci_dual_space;
+
+typedef struct {
+    int32_t q_min, q_max;
+} ltci_ambiguity;
+
+typedef struct {
+    double retain_threshold; /* keep cells with |Y| > this (strict) */
+    int32_t keep_dense;
+    int32_t threads;         /* CPU threads in the reference; ignored (results never depend on it) */
+    int32_t keystone_taps;
+    int32_t trajectory;      /* ignored by the dual-scale detectors */
+    int32_t fine_path;       /* LTCI_FINE_* (extension; AUTO picks per shape) */
+    int32_t device;          /* CUDA device ordinal (extension) */
+} ltci_options;
+
+typedef struct {
+    int32_t role, order, size;
+} ltci_axis;
+
+/* Result of one detector run.  All arrays are owned by the map and released
+ * with ltci_cuda_free_map().  Candidate and dense values are complex
+ * interleaved float64 (re, im), as ltci::DetectionMap stores them. */
+typedef struct {
+    int32_t kind;
+    int32_t n_axes;
+    ltci_axis axes[LTCI_MAX_AXES]; /* slowest first */
+    uint64_t counters[4];          /* kt, mf, ifft, fft */
+    double retain_threshold;
+    int32_t doppler_first;
+
+    uint64_t argmax;
+    double argmax_value[2];
+
+    uint64_t n_candidates;
+    uint64_t *cand_index;  /* sorted ascending */
+    double *cand_value;    /* 2 * n_candidates */
+
+    int32_t dense_stored;
+    uint64_t dense_count;
+    double *dense;         /* 2 * dense_count */
+
+    /* extension (no reference counterpart): per ROI range cell, the strongest
+     * hypothesis over all coarse/fine/Doppler cells, ties to the lowest flat
+     * index -- the per-cell peak map gathered across GPUs. */
+    int32_t n_rows;
+    uint64_t *peak_index;  /* n_rows */
+    double *peak_value;    /* 2 * n_rows */
+} ltci_detection_map;
+
+/* ---- drop-in detectors (host buffers) ---------------------------------- */
+int ltci_cuda_ds_grft(const double *cube, const ltci_radar *cube_params,
+                      const ltci_dual_space *space, const ltci_options *opt,
+                      ltci_detection_map **out);
+int ltci_cuda_ds_kt_mfp(const double *cube, const ltci_radar *cube_params,
+                        const ltci_ambiguity *amb, const ltci_dual_space *space,
+                        const ltci_options *opt, ltci_detection_map **out);
+void ltci_cuda_free_map(ltci_detection_map *map);
+
+/* ---- kernel-level secondary boundary (host buffers, float64 complex) ---- */
+int ltci_cuda_keystone(const double *cube, const ltci_radar *p, int taps, double *out);
+int ltci_cuda_mgift(const double *cube, const ltci_radar *p, const double *ctilde, int n_ctilde,
+                    int variant, double *out /* K*M complex */);
+int ltci_cuda_gft(const double *rows, const ltci_radar *p, const double *fine_higher, int n_fine,
+                  int roi_first, int roi_last, double *out /* R*M complex, (r,j) at r+R*j */);
+double ltci_cuda_detection_threshold(const ltci_radar *p, double sigma2, double pfa, int bins,
+                                     int *status);
+
+/* ---- engine: device-resident plan for streaming / benchmarking ---------- */
+typedef struct ltci_engine ltci_engine;
+
+/* variant: LTCI_VARIANT_GRFT (ds_grft) or LTCI_VARIANT_KTMFP (ds_kt_mfp; amb required).
+ * row_begin/row_end select a contiguous slice [row_begin, row_end) of the ROI
+ * rows (0 .. roi.count()) for range-cell sharding; pass 0, -1 for all rows. */
+int ltci_engine_create(const ltci_radar *p, const ltci_dual_space *space, const ltci_ambiguity *amb,
+                       int variant, const ltci_options *opt, int row_begin, int row_end,
+                       ltci_engine **out);
+void ltci_engine_destroy(ltci_engine *e);
+/* Run on a device-resident complex64 cube (K*M float2, column-major) on the
+ * given cudaStream_t (NULL = legacy default).  Asynchronous. */
+int ltci_engine_run_device(ltci_engine *e, const void *d_cube_c64, void *stream);
+/* Same from a host float64 cube: H2D, run, D2H of the reduced results. */
+int ltci_engine_run_host(ltci_engine *e, const double *cube, void *stream);
+/* Copy the reduced results of the last run to the host and build a map
+ * (synchronises the stream).  Candidates overflowing the device buffer make
+ * the engine re-run with a larger buffer, or fail with LTCI_BAD_ALLOC. */
+int ltci_engine_result(ltci_engine *e, void *stream, ltci_detection_map **out);
+/* Device pointer to the per-row peak records of the last run:
+ * n_rows records of {float re, float im, uint64 flat_index} (16 B each). */
+int ltci_engine_peaks_device(ltci_engine *e, void **d_ptr, int32_t *n_rows);
+/* Instrumentation: number of kernel launches issued by the last run, and the
+ * device time (ms) of the fine and coarse stages when timing is enabled. */
+int ltci_engine_stats(ltci_engine *e, int64_t *launches, double *fine_ms, double *coarse_ms,
+                      double *keystone_ms);
+int ltci_engine_set_timing(ltci_engine *e, int enable);
+/* hypotheses (cells) and integrations covered by this engine's row slice */
+int ltci_engine_work(ltci_engine *e, uint64_t *hypotheses, uint64_t *integrations);
+
+/* Roofline denominator for the CUDA-core fine path: dense FP32 FFMA issue
+ * rate of this device, measured with a register-resident FMA chain kernel
+ * over all SMs (TFLOP/s, 2 flop per FFMA). */
+int ltci_cuda_measure_fp32_peak(int device, double *tflops);
+
+const char *ltci_cuda_last_error(void);
+int ltci_cuda_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LTCI_CUDA_H_ */

@@ -1,0 +1,86 @@
+"""Loader for the in-tree CUDA library (lib/libltci_cuda.so).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, calls raise.  Build with ``python -c "import __graft_entry__ as g;
+g.build()"`` or ``make -C paper_2403_06788_b200/csrc all``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import _cabi as A
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libltci_cuda.so")
+DROPIN_PATH = os.path.join(LIB_DIR, "libltci_b200.so")
+
+# Every symbol include/ltci_cuda.h declares.
+EXPORTS = (
+    "ltci_cuda_ds_grft", "ltci_cuda_ds_kt_mfp", "ltci_cuda_free_map", "ltci_cuda_keystone",
+    "ltci_cuda_mgift", "ltci_cuda_gft", "ltci_cuda_detection_threshold", "ltci_engine_create",
+    "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
+    "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_work",
+    "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
+)
+
+_lib = None
+
+
+class LtciError(RuntimeError):
+    pass
+
+
+class ConditionViolated(LtciError):
+    """Mirror of ltci::ConditionViolated (proj/include/ltci/common.hpp:17-20)."""
+
+
+def raise_for(rc: int, lib) -> None:
+    if rc == A.OK:
+        return
+    msg = lib.ltci_cuda_last_error().decode(errors="replace")
+    if rc == A.INVALID_ARGUMENT:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == A.CONDITION_VIOLATED:
+        raise ConditionViolated(msg)
+    if rc == A.BAD_ALLOC:
+        raise MemoryError(msg)  # std::bad_alloc
+    raise LtciError(msg)
+
+
+def load():
+    """Load libltci_cuda.so (raises OSError when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise OSError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    vp = C.c_void_p
+    lib.ltci_cuda_ds_grft.argtypes = [vp, P(A.CRadar), P(A.CDualSpace), P(A.COptions), P(A.PMap)]
+    lib.ltci_cuda_ds_kt_mfp.argtypes = [vp, P(A.CRadar), P(A.CAmbiguity), P(A.CDualSpace), P(A.COptions),
+                                        P(A.PMap)]
+    lib.ltci_cuda_free_map.argtypes = [A.PMap]
+    lib.ltci_cuda_free_map.restype = None
+    lib.ltci_cuda_keystone.argtypes = [vp, P(A.CRadar), C.c_int, vp]
+    lib.ltci_cuda_mgift.argtypes = [vp, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, vp]
+    lib.ltci_cuda_gft.argtypes = [vp, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, C.c_int, vp]
+    lib.ltci_cuda_detection_threshold.argtypes = [P(A.CRadar), C.c_double, C.c_double, C.c_int, P(C.c_int)]
+    lib.ltci_cuda_detection_threshold.restype = C.c_double
+    lib.ltci_engine_create.argtypes = [P(A.CRadar), P(A.CDualSpace), P(A.CAmbiguity), C.c_int, P(A.COptions),
+                                       C.c_int, C.c_int, P(vp)]
+    lib.ltci_engine_destroy.argtypes = [vp]
+    lib.ltci_engine_destroy.restype = None
+    lib.ltci_engine_run_device.argtypes = [vp, vp, vp]
+    lib.ltci_engine_run_host.argtypes = [vp, vp, vp]
+    lib.ltci_engine_result.argtypes = [vp, vp, P(A.PMap)]
+    lib.ltci_engine_peaks_device.argtypes = [vp, P(vp), P(C.c_int32)]
+    lib.ltci_engine_stats.argtypes = [vp, P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_double)]
+    lib.ltci_engine_set_timing.argtypes = [vp, C.c_int]
+    lib.ltci_engine_work.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
+    lib.ltci_cuda_measure_fp32_peak.argtypes = [C.c_int, P(C.c_double)]
+    lib.ltci_cuda_last_error.restype = C.c_char_p
+    lib.ltci_cuda_version.restype = C.c_int
+    _lib = lib
+    return lib

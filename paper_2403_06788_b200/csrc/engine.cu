@@ -1,0 +1,1073 @@
+// engine.cu -- host plan, device engine and C-ABI of the B200 dual-scale
+// cascade (include/ltci_cuda.h).  One translation unit: the kernels live in
+// coarse.cuh (K1 coarse RM "gather", K4 keystone) and fine_fft.cuh (K2b fine
+// DFM stage + fused K3 reduction); fine_tc.cuh adds the tcgen05 K2a path.
+//
+// Host-side plan mirrors run_dual_scale / ds_grft / ds_kt_mfp control flow
+// (reference proj/src/detectors.cpp:337-481): coarse cells are enumerated
+// mixed-radix over the map's coarse axes (last fastest), fine cells over the
+// fine axes, the flat cell index is ((c*F + f)*R + r)*D + jj, counters follow
+// predict_counters (proj/src/bench.cpp:180-189).
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ltci_cuda.h"
+#include "coarse.cuh"
+#include "fine_fft.cuh"
+#include "fine_tc.cuh"
+
+using namespace ltcib;
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kC = 3.0e8;  // kSpeedOfLight, proj/include/ltci/common.hpp:12
+
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            fail(e_ == cudaErrorMemoryAllocation ? LTCI_BAD_ALLOC : LTCI_RUNTIME_ERROR,     \
+                 std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+    } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LTCI_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("allocation failed: ") + e.what();
+        return LTCI_BAD_ALLOC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LTCI_RUNTIME_ERROR;
+    }
+}
+
+bool is_pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
+
+double lambda_of(const ltci_radar& r) { return kC / r.fc; }
+double va_of(const ltci_radar& r) { return lambda_of(r) * r.PRF / 2.0; }
+double dR_of(const ltci_radar& r) { return kC / (2.0 * r.fs); }
+
+// RadarParams::validate (proj/src/radar_params.cpp:30-45)
+void validate_radar(const ltci_radar& p) {
+    if (!(p.fc > 0) || !(p.fs > 0) || !(p.Br > 0) || !(p.PRF > 0) || p.M <= 0 || p.K <= 0)
+        fail(LTCI_INVALID_ARGUMENT, "RadarParams: fc, fs, Br, PRF, M, K must be positive");
+    if (!is_pow2(p.M) || !is_pow2(p.K))
+        fail(LTCI_INVALID_ARGUMENT, "RadarParams: M and K must be powers of two");
+}
+
+// check_same_params (proj/src/detectors.cpp:52-55)
+void check_same_params(const ltci_radar& a, const ltci_radar& b) {
+    if (a.K != b.K || a.M != b.M || a.fc != b.fc || a.fs != b.fs || a.PRF != b.PRF)
+        fail(LTCI_INVALID_ARGUMENT, "detector: cube and search space use different radar parameters");
+}
+
+// ---------------------------------------------------------------- plan ----
+
+struct Plan {
+    ltci_radar rp{};
+    int variant = 0;
+    int P = 0;
+    std::vector<ltci_grid> coarse_axes;  // map order, last fastest
+    int q_min = 0, q_count = 1;          // KT folding axis (slowest)
+    unsigned long long coarse_cells = 1;
+    std::vector<ltci_grid> fine_axes;
+    std::vector<int> fine_orders;        // motion order of each fine axis
+    unsigned long long fine_cells = 1;
+    int n_outer = 1, n_inner = 1;
+    int R_total = 0, roi_first = 0;
+    int row_begin = 0, row_end = 0, R_slice = 0;
+    int D = 0, dop_first = 0;
+    double kappa = 1.0;
+    double retain = 0.0;
+    bool keep_dense = false;
+    int taps = 8;
+    int fine_path = LTCI_FINE_AUTO;
+    std::vector<double> cparams;          // [coarse][4]
+    std::vector<float2> h0, hstep;        // fine chirp tables
+    std::vector<ltci_axis> axes;
+    unsigned long long counters[4] = {0, 0, 0, 0};
+};
+
+// exp(+j 4pi/lambda * x) with the phase reduced in FP64 cycles
+float2 phase_lambda(double x, double lambda) {
+    const double cyc = 2.0 * x / lambda;
+    const double fr = cyc - std::nearbyint(cyc);
+    return make_float2(static_cast<float>(std::cos(2.0 * kPi * fr)), static_cast<float>(std::sin(2.0 * kPi * fr)));
+}
+
+void build_fine_tables(Plan& pl) {
+    const int M = pl.rp.M;
+    const double lam = lambda_of(pl.rp);
+    const int nf = static_cast<int>(pl.fine_axes.size());
+    pl.n_inner = nf > 0 ? pl.fine_axes[nf - 1].count : 1;
+    pl.n_outer = 1;
+    for (int i = 0; i + 1 < nf; ++i) pl.n_outer *= pl.fine_axes[i].count;
+    pl.h0.assign(static_cast<size_t>(pl.n_outer) * M, make_float2(1.f, 0.f));
+    pl.hstep.assign(M, make_float2(1.f, 0.f));
+    if (nf == 0) return;
+    for (int outer = 0; outer < pl.n_outer; ++outer) {
+        // decode outer over fine axes 0..nf-2 (last fastest)
+        std::vector<int> fi(nf, 0);
+        int rem = outer;
+        for (int i = nf - 2; i >= 0; --i) {
+            fi[i] = rem % pl.fine_axes[i].count;
+            rem /= pl.fine_axes[i].count;
+        }
+        for (int m = 0; m < M; ++m) {
+            const double t = static_cast<double>(m + 1) / pl.rp.PRF;
+            double s = 0.0;
+            for (int i = 0; i < nf; ++i) {
+                const double val = i + 1 < nf ? pl.fine_axes[i].start + pl.fine_axes[i].step * fi[i]
+                                              : pl.fine_axes[i].start;
+                s += pl.kappa * val * std::pow(t, pl.fine_orders[i]);
+            }
+            pl.h0[static_cast<size_t>(outer) * M + m] = phase_lambda(s, lam);
+        }
+    }
+    for (int m = 0; m < M; ++m) {
+        const double t = static_cast<double>(m + 1) / pl.rp.PRF;
+        pl.hstep[m] = phase_lambda(pl.kappa * pl.fine_axes[nf - 1].step * std::pow(t, pl.fine_orders[nf - 1]), lam);
+    }
+}
+
+void set_slice(Plan& pl, int row_begin, int row_end) {
+    if (row_end < 0) row_end = pl.R_total;
+    if (row_begin < 0 || row_end > pl.R_total || row_begin >= row_end)
+        fail(LTCI_INVALID_ARGUMENT, "engine: empty or out-of-range row slice");
+    pl.row_begin = row_begin;
+    pl.row_end = row_end;
+    pl.R_slice = row_end - row_begin;
+}
+
+void check_roi(const ltci_dual_space& s) {
+    const int count = s.roi_last - s.roi_first + 1;
+    // gft's check (proj/src/transforms.cpp:183-184)
+    if (count <= 0 || s.roi_first < 0 || s.roi_last >= s.radar.K)
+        fail(LTCI_INVALID_ARGUMENT, "gft: empty or out-of-range roi");
+}
+
+void check_grids(const ltci_dual_space& s) {
+    if (s.order < 1 || s.order > LTCI_MAX_ORDER)
+        fail(LTCI_INVALID_ARGUMENT, "dual-scale space: order must be in 1..4");
+    for (int p = 0; p < s.order; ++p)
+        if (s.coarse[p].count < 1 || s.fine[p].count < 1)
+            fail(LTCI_INVALID_ARGUMENT, "dual-scale space: empty grid");
+}
+
+void check_supported(const ltci_radar& r) {
+    if (r.M < 4 || r.M > 1024)
+        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: pulse count M must be a power of two in [4, 1024]");
+    if (r.K < 16 || r.K > 8192)
+        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be a power of two in [16, 8192]");
+}
+
+Plan make_plan(const ltci_radar& cube_params, const ltci_dual_space& s, const ltci_ambiguity* amb,
+               int variant, const ltci_options* opt, int row_begin, int row_end) {
+    Plan pl;
+    validate_radar(cube_params);
+    check_same_params(cube_params, s.radar);
+    pl.rp = cube_params;
+    pl.variant = variant;
+    pl.P = s.order;
+    if (variant == LTCI_VARIANT_KTMFP && s.order != 2)
+        fail(LTCI_INVALID_ARGUMENT, "ds_kt_mfp: needs a P = 2 search space");
+    if (variant == LTCI_VARIANT_KTMFP && !amb) fail(LTCI_INVALID_ARGUMENT, "ds_kt_mfp: ambiguity space required");
+    check_grids(s);
+    check_roi(s);
+    check_supported(cube_params);
+    const int M = pl.rp.M;
+    pl.kappa = s.kappa;
+    pl.R_total = s.roi_last - s.roi_first + 1;
+    pl.roi_first = s.roi_first;
+    set_slice(pl, row_begin, row_end);
+    if (opt) {
+        pl.retain = opt->retain_threshold;
+        pl.keep_dense = opt->keep_dense != 0;
+        pl.taps = opt->keystone_taps;
+        pl.fine_path = opt->fine_path;
+    }
+
+    if (variant == LTCI_VARIANT_GRFT) {
+        // ds_grft: Doppler window (proj/src/detectors.cpp:420-432)
+        const double dop_bin = va_of(pl.rp) / M;
+        int keep = static_cast<int>(std::ceil(s.kappa * s.rm_step[0] / 2.0 / dop_bin - 1e-9));
+        keep = std::min(keep, M / 2 - 1);
+        if (keep < 0) fail(LTCI_INVALID_ARGUMENT, "ds_grft: empty Doppler window");
+        pl.dop_first = M / 2 - keep;
+        pl.D = 2 * keep + 1;
+        for (int p = 0; p < s.order; ++p) pl.coarse_axes.push_back(s.coarse[p]);
+        for (int p = 2; p <= s.order; ++p) {
+            pl.fine_axes.push_back(s.fine[p - 1]);
+            pl.fine_orders.push_back(p);
+        }
+        for (int p = 1; p <= s.order; ++p) pl.axes.push_back({LTCI_AXIS_COARSE, p, s.coarse[p - 1].count});
+        for (int p = 2; p <= s.order; ++p) pl.axes.push_back({LTCI_AXIS_FINE, p, s.fine[p - 1].count});
+        pl.axes.push_back({LTCI_AXIS_RANGE, 0, pl.R_total});
+        pl.axes.push_back({LTCI_AXIS_DOPPLER, 0, pl.D});
+    } else {
+        if (pl.taps < 2) fail(LTCI_INVALID_ARGUMENT, "keystone: need at least 2 taps");
+        pl.dop_first = 0;
+        pl.D = M;
+        pl.q_min = amb->q_min;
+        pl.q_count = amb->q_max - amb->q_min + 1;
+        if (pl.q_count < 1) fail(LTCI_INVALID_ARGUMENT, "ds_kt_mfp: empty ambiguity space");
+        pl.coarse_axes.push_back(s.coarse[1]);
+        pl.fine_axes.push_back(s.fine[1]);
+        pl.fine_orders.push_back(2);
+        pl.axes.push_back({LTCI_AXIS_FOLDING, 0, pl.q_count});
+        pl.axes.push_back({LTCI_AXIS_COARSE, 2, s.coarse[1].count});
+        pl.axes.push_back({LTCI_AXIS_FINE, 2, s.fine[1].count});
+        pl.axes.push_back({LTCI_AXIS_RANGE, 0, pl.R_total});
+        pl.axes.push_back({LTCI_AXIS_DOPPLER, 0, M});
+    }
+    pl.coarse_cells = 1;
+    for (const ltci_grid& g : pl.coarse_axes) pl.coarse_cells *= static_cast<unsigned long long>(g.count);
+    if (variant == LTCI_VARIANT_KTMFP) pl.coarse_cells *= static_cast<unsigned long long>(pl.q_count);
+    pl.fine_cells = 1;
+    for (const ltci_grid& g : pl.fine_axes) pl.fine_cells *= static_cast<unsigned long long>(g.count);
+    if (pl.fine_cells * static_cast<unsigned long long>(pl.D) >= 0xffffffffull)
+        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: fine cells x Doppler bins must fit in 32 bits");
+
+    // per-coarse-cell parameters (decode exactly as run_dual_scale, detectors.cpp:360-374)
+    pl.cparams.assign(pl.coarse_cells * 4, 0.0);
+    const size_t na = pl.coarse_axes.size();
+    for (unsigned long long cidx = 0; cidx < pl.coarse_cells; ++cidx) {
+        unsigned long long rem = cidx;
+        std::vector<int> ci(na);
+        for (size_t i = na; i-- > 0;) {
+            ci[i] = static_cast<int>(rem % static_cast<unsigned long long>(pl.coarse_axes[i].count));
+            rem /= static_cast<unsigned long long>(pl.coarse_axes[i].count);
+        }
+        double* cp = &pl.cparams[cidx * 4];
+        if (variant == LTCI_VARIANT_KTMFP) {
+            cp[0] = static_cast<double>(pl.q_min + static_cast<int>(rem));
+            cp[1] = pl.coarse_axes[0].start + pl.coarse_axes[0].step * ci[0];
+        } else {
+            for (size_t i = 0; i < na; ++i) cp[i] = pl.coarse_axes[i].start + pl.coarse_axes[i].step * ci[i];
+        }
+    }
+    build_fine_tables(pl);
+
+    // predict_counters (proj/src/bench.cpp:180-189)
+    const unsigned long long Mu = static_cast<unsigned long long>(M);
+    const unsigned long long Nt = static_cast<unsigned long long>(pl.R_total);
+    if (variant == LTCI_VARIANT_GRFT) {
+        pl.counters[2] = pl.coarse_cells * Mu;
+        pl.counters[1] = pl.coarse_cells * pl.fine_cells * Nt;
+        pl.counters[3] = pl.coarse_cells * pl.fine_cells * Nt;
+    } else {
+        pl.counters[0] = 1;
+        pl.counters[2] = pl.coarse_cells * Mu;
+        pl.counters[1] = pl.coarse_cells * pl.fine_cells * Nt;
+        pl.counters[3] = pl.coarse_cells * pl.fine_cells * Nt;
+    }
+    return pl;
+}
+
+// ----------------------------------------------------------- dispatch -----
+
+void radix_plan(int K, int* radix, int* npass) {
+    int n = 0, rem = K;
+    while (rem >= 16) {
+        radix[n++] = 16;
+        rem /= 16;
+    }
+    if (rem > 1) radix[n++] = rem;
+    *npass = n;
+}
+
+int coarse_pg(int K, int M) {
+    const int Kp = K + K / 16;
+    int pg = 1;
+    while (pg < 32 && 2 * (2 * pg) * Kp * static_cast<int>(sizeof(float2)) <= 140 * 1024) pg *= 2;
+    return std::min(pg, M);
+}
+
+template <int PG>
+void launch_coarse_pg(const CoarseArgs& a, cudaStream_t st) {
+    const int Kp = a.K + a.K / 16;
+    const size_t smem = 2ull * PG * Kp * sizeof(float2);
+    auto kern = coarse_rm_kernel<PG>;
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_done = true;
+    }
+    dim3 grid(a.M / PG, a.c_count);
+    kern<<<grid, 256, smem, st>>>(a);
+    CK(cudaGetLastError());
+}
+
+void launch_coarse(const CoarseArgs& a, int pg, cudaStream_t st) {
+    switch (pg) {
+        case 1: launch_coarse_pg<1>(a, st); break;
+        case 2: launch_coarse_pg<2>(a, st); break;
+        case 4: launch_coarse_pg<4>(a, st); break;
+        case 8: launch_coarse_pg<8>(a, st); break;
+        case 16: launch_coarse_pg<16>(a, st); break;
+        default: launch_coarse_pg<32>(a, st); break;
+    }
+}
+
+template <int Q, int G, bool DENSE>
+void launch_fine_qg(const FineArgs& a, cudaStream_t st) {
+    constexpr int rows_per_block = (kFineThreads / 32) * (32 / G);
+    const size_t smem = fine_smem_floats2<Q, G>() * sizeof(float2);
+    auto kern = fine_fft_kernel<Q, G, DENSE>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_done = true;
+    }
+    const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
+    kern<<<blocks, kFineThreads, smem, st>>>(a);
+    CK(cudaGetLastError());
+}
+
+template <bool DENSE>
+void launch_fine_m(const FineArgs& a, int M, cudaStream_t st) {
+    switch (M) {
+        case 4: launch_fine_qg<4, 1, DENSE>(a, st); break;
+        case 8: launch_fine_qg<8, 1, DENSE>(a, st); break;
+        case 16: launch_fine_qg<16, 1, DENSE>(a, st); break;
+        case 32: launch_fine_qg<32, 1, DENSE>(a, st); break;
+        case 64: launch_fine_qg<32, 2, DENSE>(a, st); break;
+        case 128: launch_fine_qg<32, 4, DENSE>(a, st); break;
+        case 256: launch_fine_qg<32, 8, DENSE>(a, st); break;
+        case 512: launch_fine_qg<32, 16, DENSE>(a, st); break;
+        case 1024: launch_fine_qg<32, 32, DENSE>(a, st); break;
+        default: fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: unsupported M");
+    }
+}
+
+// --------------------------------------------------------------- engine ---
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t count) {
+        if (count <= n) return;
+        release();
+        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+}  // namespace
+
+struct ltci_engine {
+    Plan pl;
+    int device = 0;
+    DevBuf<float2> cube_c64, cube_kt, X, h0, hstep, dense;
+    DevBuf<double2> cube_f64;
+    DevBuf<double> cparams;
+    DevBuf<PeakSlot> slots;
+    DevBuf<CandRec> cand;
+    DevBuf<unsigned long long> cand_count;
+    unsigned long long cand_cap = 0;
+    unsigned long long batch = 0;  // coarse cells per X batch
+    const float2* last_cube = nullptr;
+    bool ran = false;
+    bool timing = false;
+    int64_t launches = 0;
+    double fine_ms = 0, coarse_ms = 0, keystone_ms = 0;
+    std::vector<cudaEvent_t> ev;
+    int tc_ok = -1;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev != prev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void engine_init(ltci_engine* e) {
+    const Plan& pl = e->pl;
+    const int M = pl.rp.M;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
+    if (e->device < 0 || e->device >= ndev) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad device ordinal");
+    DeviceGuard dg(e->device);
+    e->cparams.ensure(pl.cparams.size());
+    CK(cudaMemcpy(e->cparams.p, pl.cparams.data(), pl.cparams.size() * sizeof(double), cudaMemcpyHostToDevice));
+    e->h0.ensure(pl.h0.size());
+    CK(cudaMemcpy(e->h0.p, pl.h0.data(), pl.h0.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    e->hstep.ensure(pl.hstep.size());
+    CK(cudaMemcpy(e->hstep.p, pl.hstep.data(), pl.hstep.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    e->slots.ensure(pl.R_slice);
+    e->cand_count.ensure(1);
+    // X batch: bounded device footprint (default 4 GiB, LTCI_X_BUDGET_MB overrides)
+    size_t budget = 4ull << 30;
+    if (const char* env = std::getenv("LTCI_X_BUDGET_MB")) budget = std::strtoull(env, nullptr, 10) << 20;
+    const size_t per_coarse = static_cast<size_t>(pl.R_slice) * M * sizeof(float2);
+    e->batch = std::max<unsigned long long>(1, std::min<unsigned long long>(pl.coarse_cells, budget / per_coarse));
+    // the fine kernel indexes rows with int
+    e->batch = std::min<unsigned long long>(e->batch, (1ull << 30) / std::max(1, pl.R_slice));
+    e->X.ensure(e->batch * per_coarse / sizeof(float2));
+    const unsigned long long H = pl.coarse_cells * pl.fine_cells * pl.R_slice * pl.D;
+    e->cand_cap = std::max<unsigned long long>(1, std::min<unsigned long long>(H, 1ull << 22));
+    e->cand.ensure(e->cand_cap);
+    if (pl.keep_dense) {
+        const unsigned long long cells = pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D;
+        e->dense.ensure(cells);
+    }
+    if (pl.variant == LTCI_VARIANT_KTMFP) e->cube_kt.ensure(static_cast<size_t>(pl.rp.K) * M);
+}
+
+void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
+    const Plan& pl = e->pl;
+    DeviceGuard dg(e->device);
+    const int K = pl.rp.K, M = pl.rp.M;
+    e->launches = 0;
+    const bool tm = e->timing;
+    if (tm && e->ev.empty()) {
+        e->ev.resize(64);
+        for (auto& x : e->ev) CK(cudaEventCreate(&x));
+    }
+    int evi = 0;
+    std::vector<std::pair<int, int>> fine_ev, coarse_ev;
+    std::pair<int, int> kt_ev{-1, -1};
+
+    CK(cudaMemsetAsync(e->cand_count.p, 0, sizeof(unsigned long long), st));
+    {
+        // slots: re = im = 0, idx = ~0
+        std::vector<PeakSlot> init(pl.R_slice, PeakSlot{0.f, 0.f, ~0ull});
+        CK(cudaMemcpyAsync(e->slots.p, init.data(), init.size() * sizeof(PeakSlot), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));  // init lives on the host stack
+    }
+    if (pl.keep_dense) CK(cudaMemsetAsync(e->dense.p, 0, e->dense.n * sizeof(float2), st));
+
+    const float2* input = d_cube;
+    if (pl.variant == LTCI_VARIANT_KTMFP) {
+        KeystoneArgs ka;
+        ka.in = d_cube;
+        ka.out = e->cube_kt.p;
+        ka.K = K;
+        ka.M = M;
+        ka.taps = pl.taps;
+        ka.fc = pl.rp.fc;
+        ka.delta_f = pl.rp.delta_f;
+        if (tm && evi + 2 <= static_cast<int>(e->ev.size())) {
+            kt_ev = {evi, evi + 1};
+            CK(cudaEventRecord(e->ev[evi], st));
+        }
+        const size_t total = static_cast<size_t>(K) * M;
+        const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16));
+        keystone_kernel<<<blocks, 256, 0, st>>>(ka);
+        CK(cudaGetLastError());
+        ++e->launches;
+        if (kt_ev.first >= 0) {
+            CK(cudaEventRecord(e->ev[evi + 1], st));
+            evi += 2;
+        }
+        input = e->cube_kt.p;
+    }
+
+    CoarseArgs ca{};
+    ca.cube = input;
+    ca.cparams = e->cparams.p;
+    ca.X = e->X.p;
+    ca.K = K;
+    ca.M = M;
+    ca.P = pl.P;
+    ca.variant = pl.variant;
+    ca.n_base = pl.roi_first + pl.row_begin;
+    ca.R_slice = pl.R_slice;
+    ca.inv_prf = 1.0 / pl.rp.PRF;
+    ca.inv_dR = 1.0 / dR_of(pl.rp);
+    ca.two_over_lambda = 2.0 / lambda_of(pl.rp);
+    ca.Va = va_of(pl.rp);
+    ca.kt_b = -(4.0 * kPi / kC) * pl.rp.delta_f * pl.rp.delta_f / pl.rp.fc;
+    radix_plan(K, ca.radix, &ca.npass);
+    const int pg = coarse_pg(K, M);
+
+    FineArgs fa{};
+    fa.X = e->X.p;
+    fa.H0 = e->h0.p;
+    fa.Hstep = e->hstep.p;
+    fa.slots = e->slots.p;
+    fa.cand = e->cand.p;
+    fa.cand_count = e->cand_count.p;
+    fa.dense = pl.keep_dense ? e->dense.p : nullptr;
+    fa.cand_cap = e->cand_cap;
+    fa.F = pl.fine_cells;
+    fa.R_total = static_cast<unsigned long long>(pl.R_total);
+    fa.R_slice = pl.R_slice;
+    fa.row_begin = pl.row_begin;
+    fa.D = pl.D;
+    fa.dop_first = pl.dop_first;
+    {
+        const int dlo = pl.dop_first - M / 2, dhi = dlo + pl.D - 1;
+        fa.kA = dhi;
+        fa.kB = M + dlo;
+    }
+    fa.n_outer = pl.n_outer;
+    fa.n_inner = pl.n_inner;
+    {
+        const double r2 = pl.retain * pl.retain;
+        fa.retain2 = pl.retain < 0 ? -1.0f : static_cast<float>(r2);
+    }
+
+    const bool use_tc = tc_fine_selected(pl.fine_path, M, pl.D, pl.keep_dense);
+    for (unsigned long long c0 = 0; c0 < pl.coarse_cells; c0 += e->batch) {
+        const unsigned long long cc = std::min<unsigned long long>(e->batch, pl.coarse_cells - c0);
+        ca.c_begin = c0;
+        ca.c_count = static_cast<int>(cc);
+        int evc = -1;
+        if (tm && evi + 4 <= static_cast<int>(e->ev.size())) {
+            evc = evi;
+            evi += 4;
+            CK(cudaEventRecord(e->ev[evc], st));
+        }
+        launch_coarse(ca, pg, st);
+        ++e->launches;
+        if (evc >= 0) CK(cudaEventRecord(e->ev[evc + 1], st));
+        fa.c_begin = c0;
+        fa.rows = static_cast<int>(cc) * pl.R_slice;
+        if (evc >= 0) CK(cudaEventRecord(e->ev[evc + 2], st));
+        if (use_tc) {
+            e->launches += tc_fine_launch(fa, M, st);
+        } else {
+            if (pl.keep_dense)
+                launch_fine_m<true>(fa, M, st);
+            else
+                launch_fine_m<false>(fa, M, st);
+            ++e->launches;
+        }
+        if (evc >= 0) {
+            CK(cudaEventRecord(e->ev[evc + 3], st));
+            coarse_ev.push_back({evc, evc + 1});
+            fine_ev.push_back({evc + 2, evc + 3});
+        }
+    }
+    e->last_cube = d_cube;
+    e->ran = true;
+    if (tm) {
+        CK(cudaStreamSynchronize(st));
+        float ms = 0;
+        e->fine_ms = e->coarse_ms = e->keystone_ms = 0;
+        for (auto& pr : fine_ev) {
+            CK(cudaEventElapsedTime(&ms, e->ev[pr.first], e->ev[pr.second]));
+            e->fine_ms += ms;
+        }
+        for (auto& pr : coarse_ev) {
+            CK(cudaEventElapsedTime(&ms, e->ev[pr.first], e->ev[pr.second]));
+            e->coarse_ms += ms;
+        }
+        if (kt_ev.first >= 0) {
+            CK(cudaEventElapsedTime(&ms, e->ev[kt_ev.first], e->ev[kt_ev.second]));
+            e->keystone_ms = ms;
+        }
+    }
+}
+
+void upload_host_cube(ltci_engine* e, const double* cube, cudaStream_t st) {
+    const size_t n = static_cast<size_t>(e->pl.rp.K) * e->pl.rp.M;
+    e->cube_f64.ensure(n);
+    e->cube_c64.ensure(n);
+    CK(cudaMemcpyAsync(e->cube_f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice, st));
+    const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8));
+    f64_to_c64_kernel<<<blocks, 256, 0, st>>>(e->cube_f64.p, e->cube_c64.p, n);
+    CK(cudaGetLastError());
+}
+
+// exp(+j 2pi d / M) for the flat index's Doppler bin (RangeDopplerMap recentring,
+// proj/src/transforms.cpp:197-212)
+void recenter(const Plan& pl, unsigned long long idx, float re, float im, double* out) {
+    const int jj = static_cast<int>(idx % static_cast<unsigned long long>(pl.D));
+    const int d = pl.dop_first + jj - pl.rp.M / 2;
+    const double ang = 2.0 * kPi * d / pl.rp.M;
+    const double c = std::cos(ang), s = std::sin(ang);
+    out[0] = re * c - im * s;
+    out[1] = re * s + im * c;
+}
+
+void* xmalloc(size_t bytes) {
+    if (bytes == 0) return nullptr;
+    void* p = std::malloc(bytes);
+    if (!p) throw std::bad_alloc();
+    return p;
+}
+
+ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
+    const Plan& pl = e->pl;
+    DeviceGuard dg(e->device);
+    unsigned long long count = 0;
+    CK(cudaMemcpyAsync(&count, e->cand_count.p, sizeof(count), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (count > e->cand_cap) {
+        // The reference would try to hold every retained cell in host memory
+        // (24 B each); refuse what cannot fit rather than hang.
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const double host_bytes = static_cast<double>(count) * 24.0;
+        const double dev_bytes = static_cast<double>(count) * sizeof(CandRec);
+        if (dev_bytes > 0.8 * static_cast<double>(free_b) || host_bytes > 64.0 * (1ull << 30))
+            fail(LTCI_BAD_ALLOC, "ltci_cuda: " + std::to_string(count) +
+                                     " retained cells exceed the result memory (raise retain_threshold)");
+        e->cand.release();
+        e->cand_cap = count;
+        e->cand.ensure(count);
+        run_device_impl(e, e->last_cube, st);
+        CK(cudaMemcpyAsync(&count, e->cand_count.p, sizeof(count), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+
+    auto* out = static_cast<ltci_detection_map*>(std::calloc(1, sizeof(ltci_detection_map)));
+    if (!out) throw std::bad_alloc();
+    try {
+        out->kind = pl.variant == LTCI_VARIANT_GRFT ? LTCI_DS_GRFT : LTCI_DS_KT_MFP;
+        out->n_axes = static_cast<int32_t>(pl.axes.size());
+        for (size_t i = 0; i < pl.axes.size(); ++i) out->axes[i] = pl.axes[i];
+        for (int i = 0; i < 4; ++i) out->counters[i] = pl.counters[i];
+        out->retain_threshold = pl.retain;
+        out->doppler_first = pl.dop_first;
+
+        // peak slots -> per-row peaks + global argmax
+        std::vector<PeakSlot> slots(pl.R_slice);
+        CK(cudaMemcpyAsync(slots.data(), e->slots.p, slots.size() * sizeof(PeakSlot), cudaMemcpyDeviceToHost, st));
+        std::vector<CandRec> cands(count);
+        if (count)
+            CK(cudaMemcpyAsync(cands.data(), e->cand.p, count * sizeof(CandRec), cudaMemcpyDeviceToHost, st));
+        std::vector<float2> dense;
+        if (pl.keep_dense) {
+            dense.resize(e->dense.n);
+            CK(cudaMemcpyAsync(dense.data(), e->dense.p, dense.size() * sizeof(float2), cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
+
+        out->n_rows = pl.R_slice;
+        out->peak_index = static_cast<uint64_t*>(xmalloc(pl.R_slice * sizeof(uint64_t)));
+        out->peak_value = static_cast<double*>(xmalloc(2 * pl.R_slice * sizeof(double)));
+        int best = -1;
+        for (int r = 0; r < pl.R_slice; ++r) {
+            out->peak_index[r] = slots[r].idx;
+            recenter(pl, slots[r].idx, slots[r].re, slots[r].im, out->peak_value + 2 * r);
+            if (best < 0) {
+                best = r;
+                continue;
+            }
+            const float mb = mag2f(slots[best].re, slots[best].im);
+            const float mr = mag2f(slots[r].re, slots[r].im);
+            if (mr > mb || (mr == mb && slots[r].idx < slots[best].idx)) best = r;
+        }
+        out->argmax = slots[best].idx;
+        out->argmax_value[0] = out->peak_value[2 * best];
+        out->argmax_value[1] = out->peak_value[2 * best + 1];
+
+        std::sort(cands.begin(), cands.end(), [](const CandRec& a, const CandRec& b) { return a.idx < b.idx; });
+        out->n_candidates = count;
+        out->cand_index = static_cast<uint64_t*>(xmalloc(count * sizeof(uint64_t)));
+        out->cand_value = static_cast<double*>(xmalloc(2 * count * sizeof(double)));
+        for (unsigned long long i = 0; i < count; ++i) {
+            out->cand_index[i] = cands[i].idx;
+            recenter(pl, cands[i].idx, cands[i].re, cands[i].im, out->cand_value + 2 * i);
+        }
+        if (pl.keep_dense) {
+            out->dense_stored = 1;
+            out->dense_count = dense.size();
+            out->dense = static_cast<double*>(xmalloc(2 * dense.size() * sizeof(double)));
+            for (size_t i = 0; i < dense.size(); ++i) recenter(pl, i, dense[i].x, dense[i].y, out->dense + 2 * i);
+        }
+    } catch (...) {
+        ltci_cuda_free_map(out);
+        throw;
+    }
+    return out;
+}
+
+int detect(const double* cube, const ltci_radar* cp, const ltci_ambiguity* amb, const ltci_dual_space* s,
+           const ltci_options* opt, int variant, ltci_detection_map** out) {
+    return guarded([&] {
+        if (!cube || !cp || !s || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        ltci_engine eng;
+        eng.pl = make_plan(*cp, *s, amb, variant, opt, 0, -1);
+        eng.device = opt ? opt->device : 0;
+        engine_init(&eng);
+        DeviceGuard dg(eng.device);
+        cudaStream_t st = nullptr;
+        upload_host_cube(&eng, cube, st);
+        run_device_impl(&eng, eng.cube_c64.p, st);
+        *out = assemble(&eng, st);
+    });
+}
+
+}  // namespace
+
+namespace {
+
+// 8 independent FMA chains per thread keep the FMA pipe issue-bound.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = __fmaf_rn(x[i], a, b);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.678f) out[threadIdx.x] = s;  // keep the chains alive
+}
+
+}  // namespace
+
+extern "C" {
+
+int ltci_cuda_measure_fp32_peak(int device, double* tflops) {
+    return guarded([&] {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
+        DeviceGuard dg(device);
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        DevBuf<float> out;
+        out.ensure(256);
+        const int blocks = sms * 8, iters = 4096;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        ffma_peak_kernel<<<blocks, 256>>>(out.p, 64, 0.999f, 1e-4f);  // warm-up
+        CK(cudaEventRecord(e0));
+        ffma_peak_kernel<<<blocks, 256>>>(out.p, iters, 0.999f, 1e-4f);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * 256;
+        *tflops = flops / (ms * 1e-3) / 1e12;
+    });
+}
+
+const char* ltci_cuda_last_error(void) { return g_err.c_str(); }
+int ltci_cuda_version(void) { return 100; }
+
+void ltci_cuda_free_map(ltci_detection_map* m) {
+    if (!m) return;
+    std::free(m->cand_index);
+    std::free(m->cand_value);
+    std::free(m->dense);
+    std::free(m->peak_index);
+    std::free(m->peak_value);
+    std::free(m);
+}
+
+int ltci_cuda_ds_grft(const double* cube, const ltci_radar* cube_params, const ltci_dual_space* space,
+                      const ltci_options* opt, ltci_detection_map** out) {
+    return detect(cube, cube_params, nullptr, space, opt, LTCI_VARIANT_GRFT, out);
+}
+
+int ltci_cuda_ds_kt_mfp(const double* cube, const ltci_radar* cube_params, const ltci_ambiguity* amb,
+                        const ltci_dual_space* space, const ltci_options* opt, ltci_detection_map** out) {
+    return detect(cube, cube_params, amb, space, opt, LTCI_VARIANT_KTMFP, out);
+}
+
+// detection_threshold (proj/src/detectors.cpp:483-489) -- host arithmetic
+double ltci_cuda_detection_threshold(const ltci_radar* p, double sigma2, double pfa, int bins, int* status) {
+    double out = 0.0;
+    int rc = guarded([&] {
+        if (!(pfa > 0.0) || !(pfa < 1.0)) fail(LTCI_INVALID_ARGUMENT, "detection_threshold: pfa must be in (0, 1)");
+        if (sigma2 < 0) fail(LTCI_INVALID_ARGUMENT, "detection_threshold: sigma2 must be >= 0");
+        if (bins == 0) bins = p->K;
+        out = std::sqrt(-static_cast<double>(p->M) * bins * sigma2 * std::log(pfa));
+    });
+    if (status) *status = rc;
+    return out;
+}
+
+int ltci_cuda_keystone(const double* cube, const ltci_radar* p, int taps, double* out) {
+    return guarded([&] {
+        validate_radar(*p);
+        if (taps < 2) fail(LTCI_INVALID_ARGUMENT, "keystone: need at least 2 taps");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
+        const size_t n = static_cast<size_t>(p->K) * p->M;
+        DevBuf<double2> f64;
+        DevBuf<float2> a, b;
+        f64.ensure(n);
+        a.ensure(n);
+        b.ensure(n);
+        CK(cudaMemcpy(f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice));
+        f64_to_c64_kernel<<<256, 256>>>(f64.p, a.p, n);
+        KeystoneArgs ka{a.p, b.p, p->K, p->M, taps, p->fc, p->delta_f};
+        keystone_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)), 256>>>(ka);
+        CK(cudaGetLastError());
+        std::vector<float2> h(n);
+        CK(cudaMemcpy(h.data(), b.p, n * sizeof(float2), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i) {
+            out[2 * i] = h[i].x;
+            out[2 * i + 1] = h[i].y;
+        }
+    });
+}
+
+// mgift through K1 with a single coarse cell and the full range axis.
+int ltci_cuda_mgift(const double* cube, const ltci_radar* p, const double* ctilde, int n_ctilde, int variant,
+                    double* out) {
+    return guarded([&] {
+        validate_radar(*p);
+        check_supported(*p);
+        if (variant == LTCI_VARIANT_KTMFP && n_ctilde != 2) fail(LTCI_INVALID_ARGUMENT, "build_mf: KtRm needs [q, c2]");
+        if (variant == LTCI_VARIANT_GRFT && (n_ctilde < 1 || n_ctilde > 4))
+            fail(LTCI_INVALID_ARGUMENT, "build_mf: RM needs c1..cP");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
+        const int K = p->K, M = p->M;
+        const size_t n = static_cast<size_t>(K) * M;
+        DevBuf<double2> f64;
+        DevBuf<float2> a, X;
+        DevBuf<double> cpar;
+        f64.ensure(n);
+        a.ensure(n);
+        X.ensure(n);
+        cpar.ensure(4);
+        double cp4[4] = {0, 0, 0, 0};
+        for (int i = 0; i < n_ctilde; ++i) cp4[i] = ctilde[i];
+        CK(cudaMemcpy(cpar.p, cp4, sizeof(cp4), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice));
+        f64_to_c64_kernel<<<256, 256>>>(f64.p, a.p, n);
+        CoarseArgs ca{};
+        ca.cube = a.p;
+        ca.cparams = cpar.p;
+        ca.X = X.p;
+        ca.c_begin = 0;
+        ca.c_count = 1;
+        ca.K = K;
+        ca.M = M;
+        ca.P = variant == LTCI_VARIANT_GRFT ? n_ctilde : 2;
+        ca.variant = variant;
+        ca.n_base = 0;
+        ca.R_slice = K;
+        ca.inv_prf = 1.0 / p->PRF;
+        ca.inv_dR = 1.0 / dR_of(*p);
+        ca.two_over_lambda = 2.0 / lambda_of(*p);
+        ca.Va = va_of(*p);
+        ca.kt_b = -(4.0 * kPi / kC) * p->delta_f * p->delta_f / p->fc;
+        radix_plan(K, ca.radix, &ca.npass);
+        launch_coarse(ca, coarse_pg(K, M), nullptr);
+        std::vector<float2> h(n);
+        CK(cudaMemcpy(h.data(), X.p, n * sizeof(float2), cudaMemcpyDeviceToHost));
+        // X[n][m] -> RangePulseCube data[n + K*m]
+        for (int m = 0; m < M; ++m)
+            for (int r = 0; r < K; ++r) {
+                out[2 * (r + static_cast<size_t>(K) * m)] = h[static_cast<size_t>(r) * M + m].x;
+                out[2 * (r + static_cast<size_t>(K) * m) + 1] = h[static_cast<size_t>(r) * M + m].y;
+            }
+    });
+}
+
+// gft through the fine kernel: one "coarse cell", one fine cell with the
+// caller's higher-order values, full Doppler axis, dense output.
+int ltci_cuda_gft(const double* rows, const ltci_radar* p, const double* fine_higher, int n_fine, int roi_first,
+                  int roi_last, double* out) {
+    return guarded([&] {
+        validate_radar(*p);
+        check_supported(*p);
+        const int R = roi_last - roi_first + 1;
+        if (R <= 0 || roi_first < 0 || roi_last >= p->K) fail(LTCI_INVALID_ARGUMENT, "gft: empty or out-of-range roi");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
+        const int K = p->K, M = p->M;
+        // rows[n + K*m] -> X[r][m] in complex64
+        std::vector<float2> hx(static_cast<size_t>(R) * M);
+        for (int r = 0; r < R; ++r)
+            for (int m = 0; m < M; ++m) {
+                const size_t src = 2 * (static_cast<size_t>(roi_first + r) + static_cast<size_t>(K) * m);
+                hx[static_cast<size_t>(r) * M + m] = make_float2(static_cast<float>(rows[src]), static_cast<float>(rows[src + 1]));
+            }
+        const double lam = lambda_of(*p);
+        std::vector<float2> h0(M), hs(M, make_float2(1.f, 0.f));
+        for (int m = 0; m < M; ++m) {
+            const double t = static_cast<double>(m + 1) / p->PRF;
+            double s = 0, tp = t;
+            for (int i = 0; i < n_fine; ++i) {
+                tp *= t;
+                s += fine_higher[i] * tp;
+            }
+            h0[m] = phase_lambda(s, lam);
+        }
+        DevBuf<float2> X, H0, HS, dense;
+        DevBuf<PeakSlot> slots;
+        DevBuf<CandRec> cand;
+        DevBuf<unsigned long long> cnt;
+        X.ensure(hx.size());
+        H0.ensure(M);
+        HS.ensure(M);
+        dense.ensure(static_cast<size_t>(R) * M);
+        slots.ensure(R);
+        cand.ensure(1);
+        cnt.ensure(1);
+        CK(cudaMemcpy(X.p, hx.data(), hx.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(H0.p, h0.data(), M * sizeof(float2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(HS.p, hs.data(), M * sizeof(float2), cudaMemcpyHostToDevice));
+        CK(cudaMemset(cnt.p, 0, sizeof(unsigned long long)));
+        CK(cudaMemset(slots.p, 0, R * sizeof(PeakSlot)));
+        FineArgs fa{};
+        fa.X = X.p;
+        fa.H0 = H0.p;
+        fa.Hstep = HS.p;
+        fa.slots = slots.p;
+        fa.cand = cand.p;
+        fa.cand_count = cnt.p;
+        fa.dense = dense.p;
+        fa.cand_cap = 0;
+        fa.c_begin = 0;
+        fa.F = 1;
+        fa.R_total = R;
+        fa.rows = R;
+        fa.R_slice = R;
+        fa.row_begin = 0;
+        fa.D = M;
+        fa.dop_first = 0;
+        fa.kA = M / 2 - 1;
+        fa.kB = M / 2;
+        fa.n_outer = 1;
+        fa.n_inner = 1;
+        fa.retain2 = INFINITY;
+        launch_fine_m<true>(fa, M, nullptr);
+        std::vector<float2> hd(static_cast<size_t>(R) * M);
+        CK(cudaMemcpy(hd.data(), dense.p, hd.size() * sizeof(float2), cudaMemcpyDeviceToHost));
+        // dense[r*M + j] -> map data[r + R*j] with the recentring twiddle
+        for (int r = 0; r < R; ++r)
+            for (int j = 0; j < M; ++j) {
+                const float2 v = hd[static_cast<size_t>(r) * M + j];
+                const double ang = 2.0 * kPi * (j - M / 2) / M;
+                const double c = std::cos(ang), s = std::sin(ang);
+                const size_t o = 2 * (static_cast<size_t>(r) + static_cast<size_t>(R) * j);
+                out[o] = v.x * c - v.y * s;
+                out[o + 1] = v.x * s + v.y * c;
+            }
+    });
+}
+
+int ltci_engine_create(const ltci_radar* p, const ltci_dual_space* space, const ltci_ambiguity* amb, int variant,
+                       const ltci_options* opt, int row_begin, int row_end, ltci_engine** out) {
+    return guarded([&] {
+        if (!p || !space || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        auto* e = new ltci_engine();
+        try {
+            e->pl = make_plan(*p, *space, amb, variant, opt, row_begin, row_end);
+            e->device = opt ? opt->device : 0;
+            engine_init(e);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
+void ltci_engine_destroy(ltci_engine* e) {
+    if (!e) return;
+    {
+        DeviceGuard dg(e->device);
+        for (auto& x : e->ev) cudaEventDestroy(x);
+        e->ev.clear();
+        delete e;
+    }
+}
+
+int ltci_engine_run_device(ltci_engine* e, const void* d_cube_c64, void* stream) {
+    return guarded([&] {
+        if (!e || !d_cube_c64) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        run_device_impl(e, static_cast<const float2*>(d_cube_c64), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ltci_engine_run_host(ltci_engine* e, const double* cube, void* stream) {
+    return guarded([&] {
+        if (!e || !cube) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        DeviceGuard dg(e->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        upload_host_cube(e, cube, st);
+        run_device_impl(e, e->cube_c64.p, st);
+        e->launches += 1;  // conversion kernel
+    });
+}
+
+int ltci_engine_result(ltci_engine* e, void* stream, ltci_detection_map** out) {
+    return guarded([&] {
+        if (!e || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        if (!e->ran) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: engine has not run");
+        *out = assemble(e, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ltci_engine_peaks_device(ltci_engine* e, void** d_ptr, int32_t* n_rows) {
+    return guarded([&] {
+        if (!e || !d_ptr || !n_rows) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        *d_ptr = e->slots.p;
+        *n_rows = e->pl.R_slice;
+    });
+}
+
+int ltci_engine_stats(ltci_engine* e, int64_t* launches, double* fine_ms, double* coarse_ms, double* keystone_ms) {
+    return guarded([&] {
+        if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        if (launches) *launches = e->launches;
+        if (fine_ms) *fine_ms = e->fine_ms;
+        if (coarse_ms) *coarse_ms = e->coarse_ms;
+        if (keystone_ms) *keystone_ms = e->keystone_ms;
+    });
+}
+
+int ltci_engine_set_timing(ltci_engine* e, int enable) {
+    return guarded([&] {
+        if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        e->timing = enable != 0;
+    });
+}
+
+int ltci_engine_work(ltci_engine* e, uint64_t* hypotheses, uint64_t* integrations) {
+    return guarded([&] {
+        if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        const Plan& pl = e->pl;
+        const unsigned long long H = pl.coarse_cells * pl.fine_cells * pl.R_slice * pl.D;
+        if (hypotheses) *hypotheses = H;
+        if (integrations) *integrations = H * static_cast<unsigned long long>(pl.rp.M);
+    });
+}
+
+}  // extern "C"

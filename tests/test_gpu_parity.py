@@ -1,0 +1,267 @@
+"""GPU parity through the C-ABI (lib/libltci_cuda.so) against the oracle:
+the reference's own outputs (golden vectors from oracle/_ref) and our C
+restatement (oracle/liboracle.so) on the same seeded complex64 inputs.
+
+Tolerances (north star, BASELINE.json): magnitudes within 1e-3 relative to
+the compared set's largest magnitude (dense maps) or to the value itself
+(candidates, peaks); indices identical except ties within 1e-3.  The kernel
+level transforms are held much tighter (FP32 FFT class, 2e-5)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2403_06788_b200 import (AmbiguitySpace, DetectorOptions, ds_grft, ds_kt_mfp, gft, keystone, mgift)
+from paper_2403_06788_b200 import scene
+from paper_2403_06788_b200.configs import baseline_space, config
+from paper_2403_06788_b200.detectors import Engine
+from paper_2403_06788_b200.model import Bounds, RadarParams, RangeRoi, build_ambiguity
+
+from helpers import TOL, check_candidates, check_peaks, cube, load, max_rel, radar, space
+
+pytestmark = pytest.mark.gpu
+
+KTOL = 2e-5  # kernel-level transforms (FP32 FFT accuracy)
+
+
+# ------------------------------------------------------------- kernels ---
+def test_mgift_matches_reference_golden():
+    g = load("transforms.npz")
+    p = radar(g)
+    x = cube(g)
+    assert max_rel(mgift(x, p, [11.7, -4.1]), g["mgift"]) < KTOL
+    d = mgift(x, p, [11.7, -4.1]) - g["mgift"]
+    assert np.abs(d).max() / np.abs(g["mgift"]).max() < KTOL
+    d = mgift(x, p, [2.0, 3.3], 1) - g["mgift_kt"]
+    assert np.abs(d).max() / np.abs(g["mgift_kt"]).max() < KTOL
+
+
+def test_gft_matches_reference_golden():
+    g = load("transforms.npz")
+    p = radar(g)
+    y = gft(g["rows"], p, [1.2], 1, p.K - 2)
+    d = y - g["gft"]
+    assert np.abs(d).max() / np.abs(g["gft"]).max() < KTOL
+
+
+def test_keystone_matches_reference_golden():
+    g = load("transforms.npz")
+    p = radar(g)
+    for taps, key in ((8, "keystone"), (4, "keystone4")):
+        d = keystone(cube(g), p, taps) - g[key]
+        assert np.abs(d).max() / np.abs(g[key]).max() < KTOL
+
+
+@pytest.mark.parametrize("M,K", [(4, 16), (8, 32), (16, 64), (32, 64), (64, 128), (128, 256), (256, 512),
+                                 (512, 1024), (1024, 2048)])
+def test_transforms_all_sizes(M, K):
+    p = RadarParams.create(3e9, 20e6, 18e6, 1000.0, M, K)
+    x = scene.to_complex64_roundtrip(scene.add_noise(np.zeros((M, K), complex), 1.0, M + K))
+    for c, v in (([123.0, -7.5], 0), ([41.0, 3.0, 0.4], 0), ([3.0, 6.5], 1)):
+        ref = O.port_mgift(x, p, c, v)
+        assert np.abs(mgift(x, p, c, v) - ref).max() / np.abs(ref).max() < KTOL
+    rows = scene.to_complex64_roundtrip(O.port_mgift(x, p, [0.0]))
+    for fine in ([], [1.7], [0.9, -0.3]):
+        ref = O.port_gft(rows, p, fine, 1, K - 2)
+        assert np.abs(gft(rows, p, fine, 1, K - 2) - ref).max() / np.abs(ref).max() < KTOL
+    ref = O.port_keystone(x, p, 8)
+    assert np.abs(keystone(x, p, 8) - ref).max() / np.abs(ref).max() < KTOL
+
+
+# ------------------------------------------------------------ detectors ---
+def _check_map(gm, g, prefix="", retain=None, value_at=None):
+    assert gm.counters == tuple(int(c) for c in g[prefix + "counters"])
+    assert [[a.role, a.order, a.size] for a in gm.axes] == g[prefix + "axes"].tolist()
+    assert gm.doppler_first == int(g[prefix + "doppler_first"])
+    if prefix + "dense" in g:
+        ref = g[prefix + "dense"]
+        assert gm.dense_stored and gm.dense.shape == ref.shape
+        assert max_rel(gm.dense, ref) <= TOL
+        # the complex values themselves, not only magnitudes
+        assert np.abs(gm.dense - ref).max() / np.abs(ref).max() <= TOL
+    ref_max = abs(complex(g[prefix + "argmax_value"]))
+    if gm.argmax != int(g[prefix + "argmax"]):
+        assert value_at is not None, "argmax index differs"
+        assert abs(abs(value_at(gm.argmax)) - ref_max) <= TOL * ref_max
+    assert abs(abs(gm.argmax_value) - ref_max) <= TOL * ref_max
+    if retain is not None:
+        check_candidates(gm.cand_index, gm.cand_value, g[prefix + "cand_index"], g[prefix + "cand_value"], retain)
+
+
+def test_ds_grft_small_golden():
+    g = load("small_grft.npz")
+    p = radar(g)
+    s = space(g, p)
+    gm = ds_grft(cube(g), p, s, DetectorOptions(retain_threshold=float(g["retain"]), keep_dense=True))
+    dense_ref = g["dense"]
+    _check_map(gm, g, retain=float(g["retain"]), value_at=lambda i: dense_ref[i])
+    check_peaks(gm.peak_index, gm.peak_value, g["peak_index"], g["peak_value"], value_at=lambda i: dense_ref[i])
+
+
+def test_ds_kt_mfp_small_golden():
+    g = load("small_kt.npz")
+    p = radar(g)
+    s = space(g, p)
+    amb = AmbiguitySpace(int(g["amb"][0]), int(g["amb"][1]))
+    gm = ds_kt_mfp(cube(g), p, amb, s, DetectorOptions(retain_threshold=float(g["retain"]), keep_dense=True))
+    dense_ref = g["dense"]
+    _check_map(gm, g, retain=float(g["retain"]), value_at=lambda i: dense_ref[i])
+    check_peaks(gm.peak_index, gm.peak_value, g["peak_index"], g["peak_value"], value_at=lambda i: dense_ref[i])
+
+
+def test_order_one_and_three_golden():
+    g = load("p1_p3.npz")
+    p = radar(g)
+    for pre in ("1", "3"):
+        s = space(g, p, f"s{pre}_")
+        gm = ds_grft(cube(g), p, s, DetectorOptions(retain_threshold=1.0, keep_dense=True))
+        dense_ref = g[f"m{pre}_dense"]
+        _check_map(gm, g, prefix=f"m{pre}_", retain=1.0, value_at=lambda i: dense_ref[i])
+
+
+def test_c0_full_config_golden():
+    """BASELINE config 0 end to end: candidates above the Pfa=1e-6 threshold,
+    global argmax, counters and the per-range-cell peak map."""
+    g = load("c0.npz")
+    w = config(0)
+    x = cube(g)
+    gamma = float(g["gamma"])
+    gm = ds_grft(x, w.params, w.space, DetectorOptions(retain_threshold=gamma))
+
+    def value_at(idx):
+        return _cell_value(x, w, idx)
+
+    _check_map(gm, g, retain=gamma, value_at=value_at)
+    ties = check_peaks(gm.peak_index, gm.peak_value, g["peak_index"], g["peak_value"], value_at=value_at)
+    assert ties <= 3
+
+
+def _cell_value(x, w, idx):
+    """Oracle value of one DS-GRFT flat cell via the C restatement."""
+    from paper_2403_06788_b200.configs import doppler_window
+    p, s = w.params, w.space
+    first, D = doppler_window(p, s)
+    R = s.roi.count()
+    F = int(np.prod([g.count for g in s.fine[1:]])) if s.order() > 1 else 1
+    jj = idx % D
+    r = (idx // D) % R
+    f = (idx // (D * R)) % F
+    c = idx // (D * R * F)
+    ci, rem = [], c
+    for gax in reversed(s.coarse):
+        ci.append(rem % gax.count)
+        rem //= gax.count
+    ci = ci[::-1]
+    cv = [float(s.coarse[i].value(ci[i])) for i in range(s.order())]
+    fi, rem = [], f
+    for gax in reversed(s.fine[1:]):
+        fi.append(rem % gax.count)
+        rem //= gax.count
+    fi = fi[::-1]
+    fine = [s.kappa * float(s.fine[i + 1].value(fi[i])) for i in range(s.order() - 1)]
+    rows = O.port_mgift(x, p, cv)
+    y = O.port_gft(rows, p, fine, s.roi.first + r, s.roi.first + r)
+    return complex(y[first + jj, 0])
+
+
+def test_c0_noiseless_recovers_target():
+    """Appendix C step 5: noiseless C0 focuses at cell 200, v ~ 87.12, c2 ~ 1.867."""
+    w = config(0)
+    x = scene.to_complex64_roundtrip(w.cube(noise=False))
+    gm = ds_grft(x, w.params, w.space, DetectorOptions(retain_threshold=1e9))
+    cell = gm.decode(gm.argmax)
+    p, s = w.params, w.space
+    vd = (gm.doppler_first + cell[4] - p.M / 2.0) * p.Va() / p.M
+    v = float(s.coarse[0].value(cell[0])) + vd / s.kappa
+    c2 = float(s.coarse[1].value(cell[1])) + float(s.fine[1].value(cell[2]))
+    assert cell[3] == 200
+    assert abs(v - 87.12) < 0.05 and abs(c2 - 1.867) < 0.01
+
+
+def test_ds_grft_random_spaces_vs_port():
+    """Reference-built spaces over several (K, M, fc/fs) shapes, dense compare."""
+    rng = np.random.default_rng(5)
+    for K, M, ratio in ((64, 16, 4.0), (128, 32, 8.0), (64, 64, 4.0), (256, 128, 16.0)):
+        p = RadarParams.create(ratio * 100e6, 100e6, 50e6, 2000.0, M, K)
+        from paper_2403_06788_b200.model import build_dual_scale
+        s = build_dual_scale(p, 2, [Bounds(-30.0, 30.0), Bounds(-8.0, 8.0)], [0.5, 0.5],
+                             RangeRoi(int(rng.integers(0, K // 4)), K - 1 - int(rng.integers(0, K // 4))))
+        x = scene.to_complex64_roundtrip(
+            scene.add_noise(scene.synthesize_cube(p, [(0.3, [K / 2 * p.delta_R(), 11.0, 2.5])]), 1.0 / K, K + M))
+        opt = DetectorOptions(retain_threshold=0.5, keep_dense=True)
+        gm = ds_grft(x, p, s, opt)
+        rm = O.port_ds(x, p, s, opt)
+        assert gm.counters == rm.counters
+        assert max_rel(gm.dense, rm.dense) <= TOL
+        check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, 0.5)
+        check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
+        amb = build_ambiguity(p, Bounds(-1.6 * p.Va(), 1.6 * p.Va()))
+        gk = ds_kt_mfp(x, p, amb, s, opt)
+        rk = O.port_ds(x, p, s, opt, 1, amb)
+        assert max_rel(gk.dense, rk.dense) <= TOL
+        check_peaks(gk.peak_index, gk.peak_value, rk.peak_index, rk.peak_value, value_at=lambda i: rk.dense[i])
+
+
+# --------------------------------------------------------------- edges ---
+def test_zero_cube_and_default_retain():
+    p = RadarParams.create(8e8, 100e6, 50e6, 2000.0, 32, 64)
+    s = baseline_space(p, [(-40.0, 40.0), (-15.0, 15.0)])
+    gm = ds_grft(np.zeros((p.M, p.K), complex), p, s)
+    assert gm.argmax == 0 and gm.argmax_value == 0 and gm.cand_index.size == 0
+    # default retain 0 keeps every nonzero cell: equals the dense cell count
+    x = scene.to_complex64_roundtrip(scene.add_noise(np.zeros((p.M, p.K), complex), 1.0, 3))
+    gm = ds_grft(x, p, s, DetectorOptions(keep_dense=True))
+    assert gm.cand_index.size == gm.cell_count() == gm.dense.size
+
+
+def test_errors_mirror_reference():
+    p = RadarParams.create(8e8, 100e6, 50e6, 2000.0, 32, 64)
+    s = baseline_space(p, [(-40.0, 40.0), (-15.0, 15.0)])
+    x = np.zeros((p.M, p.K), complex)
+    q = RadarParams.create(8e8, 100e6, 50e6, 1000.0, 32, 64)
+    with pytest.raises(ValueError, match="different radar parameters"):
+        ds_grft(x, q, s)
+    s3 = baseline_space(p, [(-40.0, 40.0), (-15.0, 15.0), (-1.0, 1.0)])
+    with pytest.raises(ValueError, match="P = 2"):
+        ds_kt_mfp(x, p, AmbiguitySpace(-1, 1), s3)
+    bad = baseline_space(p, [(-40.0, 40.0), (-15.0, 15.0)], roi=RangeRoi(5, 4))
+    with pytest.raises(ValueError, match="roi"):
+        ds_grft(x, p, bad)
+    with pytest.raises(ValueError, match="taps"):
+        ds_kt_mfp(x, p, AmbiguitySpace(-1, 1), s, DetectorOptions(keystone_taps=1))
+
+
+def test_deterministic_and_sharded_engines_merge_to_full():
+    """Range-cell shards (the multi-GPU partition) merge to the full map bit-exactly."""
+    w = config(0)
+    x = scene.to_complex64_roundtrip(w.cube())
+    gamma = 60.0
+    opt = DetectorOptions(retain_threshold=gamma)
+    full = Engine(w.params, w.space, opt=opt)
+    full.run_host(x)
+    a = full.result()
+    full.run_host(x)
+    b = full.result()
+    assert a.argmax == b.argmax and np.array_equal(a.peak_index, b.peak_index)
+    assert np.array_equal(a.peak_value, b.peak_value) and np.array_equal(a.cand_index, b.cand_index)
+    R = w.space.roi.count()
+    cuts = [0, 100, 257, R]
+    pi, pv, ci = [], [], []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        e = Engine(w.params, w.space, opt=opt, row_begin=lo, row_end=hi)
+        e.run_host(x)
+        m = e.result()
+        pi.append(m.peak_index)
+        pv.append(m.peak_value)
+        ci.append(m.cand_index)
+    assert np.array_equal(np.concatenate(pi), a.peak_index)
+    assert np.array_equal(np.concatenate(pv), a.peak_value)
+    assert np.array_equal(np.sort(np.concatenate(ci)), a.cand_index)
+
+
+def test_dropin_library_loads():
+    import ctypes
+    from paper_2403_06788_b200 import _lib
+    lib = ctypes.CDLL(_lib.DROPIN_PATH)
+    assert lib is not None
