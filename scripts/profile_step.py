@@ -1,0 +1,29 @@
+"""One engine pass over a BASELINE workload (for ncu / compute-sanitizer runs)."""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2403_06788_b200 import _cabi as A, configs, scene  # noqa: E402
+from paper_2403_06788_b200.detectors import Engine, detection_threshold  # noqa: E402
+from paper_2403_06788_b200.model import DetectorOptions  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=1)
+ap.add_argument("--runs", type=int, default=1)
+ap.add_argument("--fine-path", default="auto", choices=["auto", "fft", "tc"])
+ap.add_argument("--coarse-v", type=int, default=0, help="slice the coarse velocity axis")
+a = ap.parse_args()
+w = configs.config(a.config)
+if a.coarse_v:
+    w = configs.sliced(w, a.coarse_v)
+fp = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE}[a.fine_path]
+opt = DetectorOptions(retain_threshold=detection_threshold(w.params, w.sigma2, 1e-6), fine_path=fp)
+e = Engine(w.params, w.space, w.variant, w.amb, opt)
+x = scene.to_complex64_roundtrip(w.cube())
+for _ in range(a.runs):
+    e.run_host(x)
+m = e.result()
+print(w.name, "argmax", m.argmax, abs(m.argmax_value), "candidates", m.cand_index.size, e.stats())
