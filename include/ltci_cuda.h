@@ -76,7 +76,8 @@ enum { LTCI_VARIANT_GRFT = 0, LTCI_VARIANT_KTMFP = 1 };
 enum {
     LTCI_FINE_AUTO = 0,
     LTCI_FINE_FFT_CUDA_CORE = 1, /* chirp recurrence + register/smem FFT, FP32   */
-    LTCI_FINE_TC_DENSE = 2       /* tcgen05 dense complex contraction, fp16 split */
+    LTCI_FINE_TC_DENSE = 2,      /* tcgen05 dense complex contraction, 3-term fp16 split (FP32 class) */
+    LTCI_FINE_TC_FAST = 3        /* tcgen05, single fp16 term (~3e-4 of the row max; opt-in) */
 };
 
 typedef struct {

@@ -14,7 +14,7 @@ OK, INVALID_ARGUMENT, CONDITION_VIOLATED, RUNTIME_ERROR, BAD_ALLOC, NO_DEVICE = 
 FD_GRFT, TD_GRFT, KT_MFP, DS_GRFT, DS_KT_MFP = range(5)
 AXIS_RANGE, AXIS_VELOCITY, AXIS_HIGHER, AXIS_DOPPLER, AXIS_COARSE, AXIS_FINE, AXIS_FOLDING = range(7)
 VARIANT_GRFT, VARIANT_KTMFP = 0, 1
-FINE_AUTO, FINE_FFT_CUDA_CORE, FINE_TC_DENSE = 0, 1, 2
+FINE_AUTO, FINE_FFT_CUDA_CORE, FINE_TC_DENSE, FINE_TC_FAST = 0, 1, 2, 3
 
 
 class CRadar(C.Structure):

@@ -15,6 +15,8 @@
 // (X[row][m]), which is the K-major layout the fine stage streams.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace ltcib {
@@ -22,7 +24,10 @@ namespace ltcib {
 struct CoarseArgs {
     const float2* cube;      // K x M complex64, column-major (k + K*m)
     const double* cparams;   // [coarse][4]: GRFT c1..cP ; KT (q, c2)
-    float2* X;               // [c_count * R_slice][M]
+    float2* X;               // [c_count * R_slice][M]          (OUT16 = 0)
+    uint32_t* Xh;            // [c_count * R_slice][M] half2 hi  (OUT16 = 1, tcgen05 path)
+    uint32_t* Xl;            // [c_count * R_slice][M] half2 lo
+    const unsigned* maxbits; // max |y|^2 for the fp16 prescale (OUT16 = 1)
     unsigned long long c_begin;
     int c_count;
     int K, M, P, variant;
@@ -68,8 +73,18 @@ __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, flo
     }
 }
 
+// Power-of-two prescale mapping the worst-case |X| <= K max|y| near 2^15
+// (fp16 hi/lo operands of the tensor-core fine path).
+__device__ __forceinline__ float fp16_prescale(const unsigned* maxbits, int K) {
+    const float m2 = __uint_as_float(*maxbits);
+    if (!(m2 > 0.f)) return 1.0f;
+    const float bound = static_cast<float>(K) * sqrtf(m2);
+    const int e = static_cast<int>(floorf(log2f(30000.0f / bound)));
+    return ldexpf(1.0f, max(-60, min(60, e)));
+}
+
 // grid: (M / PG, c_count); block 256
-template <int PG>
+template <int PG, int OUT16>
 __global__ void __launch_bounds__(256) coarse_rm_kernel(CoarseArgs a) {
     extern __shared__ float2 smem[];
     const int K = a.K;
@@ -153,13 +168,26 @@ __global__ void __launch_bounds__(256) coarse_rm_kernel(CoarseArgs a) {
     }
 
     // shifted ROI store, pulse-contiguous rows
-    float2* Xc = a.X + static_cast<size_t>(c_local) * a.R_slice * a.M;
+    const size_t cbase = static_cast<size_t>(c_local) * a.R_slice * a.M;
+    const float sc = OUT16 ? fp16_prescale(a.maxbits, K) : 1.0f;
     for (int idx = tid; idx < a.R_slice * PG; idx += blockDim.x) {
         const int r = idx / PG;
         const int p = idx - r * PG;
         int n = a.n_base + r + s_shift[p];
         n &= K - 1;
-        Xc[static_cast<size_t>(r) * a.M + m0 + p] = cmul(in[p * Kp + padi(n)], s_pre[p]);
+        const float2 v = cmul(in[p * Kp + padi(n)], s_pre[p]);
+        const size_t o = cbase + static_cast<size_t>(r) * a.M + m0 + p;
+        if (OUT16) {
+            // x = x_hi + x_lo in fp16 (interleaved re, im along K)
+            const float xr = v.x * sc, xi = v.y * sc;
+            __half2 hi = __floats2half2_rn(xr, xi);
+            const float2 hf = __half22float2(hi);
+            __half2 lo = __floats2half2_rn(xr - hf.x, xi - hf.y);
+            a.Xh[o] = *reinterpret_cast<uint32_t*>(&hi);
+            a.Xl[o] = *reinterpret_cast<uint32_t*>(&lo);
+        } else {
+            a.X[o] = v;
+        }
     }
 }
 

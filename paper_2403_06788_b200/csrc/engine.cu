@@ -307,11 +307,11 @@ int coarse_pg(int K, int M) {
     return std::min(pg, M);
 }
 
-template <int PG>
+template <int PG, int OUT16>
 void launch_coarse_pg(const CoarseArgs& a, cudaStream_t st) {
     const int Kp = a.K + a.K / 16;
     const size_t smem = 2ull * PG * Kp * sizeof(float2);
-    auto kern = coarse_rm_kernel<PG>;
+    auto kern = coarse_rm_kernel<PG, OUT16>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -322,15 +322,66 @@ void launch_coarse_pg(const CoarseArgs& a, cudaStream_t st) {
     CK(cudaGetLastError());
 }
 
-void launch_coarse(const CoarseArgs& a, int pg, cudaStream_t st) {
+template <int OUT16>
+void launch_coarse_out(const CoarseArgs& a, int pg, cudaStream_t st) {
     switch (pg) {
-        case 1: launch_coarse_pg<1>(a, st); break;
-        case 2: launch_coarse_pg<2>(a, st); break;
-        case 4: launch_coarse_pg<4>(a, st); break;
-        case 8: launch_coarse_pg<8>(a, st); break;
-        case 16: launch_coarse_pg<16>(a, st); break;
-        default: launch_coarse_pg<32>(a, st); break;
+        case 1: launch_coarse_pg<1, OUT16>(a, st); break;
+        case 2: launch_coarse_pg<2, OUT16>(a, st); break;
+        case 4: launch_coarse_pg<4, OUT16>(a, st); break;
+        case 8: launch_coarse_pg<8, OUT16>(a, st); break;
+        case 16: launch_coarse_pg<16, OUT16>(a, st); break;
+        default: launch_coarse_pg<32, OUT16>(a, st); break;
     }
+}
+
+void launch_coarse(const CoarseArgs& a, int pg, cudaStream_t st, bool out16 = false) {
+    if (out16)
+        launch_coarse_out<1>(a, pg, st);
+    else
+        launch_coarse_out<0>(a, pg, st);
+}
+
+// ---- tcgen05 fine path: TMA tensor maps over the fp16 X planes ----------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) fail(LTCI_RUNTIME_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// [rows][2M] fp16, box 64 (K) x 256 (rows), 128-byte swizzle (matches sw128_desc)
+CUtensorMap make_x16_map(void* base, int M, unsigned long long rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * M), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * M) * 2};
+    const cuuint32_t box[2] = {TC_BK, TC_BN};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LTCI_RUNTIME_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+template <int TERMS>
+void launch_tc_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& lo, cudaStream_t st) {
+    auto kern = fine_tc_kernel<TERMS>;
+    const size_t smem = tc_smem_bytes(TERMS, a.tab_f, a.M);
+    if (smem > 227 * 1024) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: tcgen05 tile tables exceed shared memory");
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const int Q = static_cast<int>(a.f.F) * a.f.D;
+    dim3 grid((Q + TC_QT - 1) / TC_QT, (a.f.rows + TC_BN - 1) / TC_BN);
+    kern<<<grid, TC_THREADS, smem, st>>>(a, hi, lo);
+    CK(cudaGetLastError());
 }
 
 template <int Q, int G, bool DENSE>
@@ -403,7 +454,12 @@ struct ltci_engine {
     int64_t launches = 0;
     double fine_ms = 0, coarse_ms = 0, keystone_ms = 0;
     std::vector<cudaEvent_t> ev;
-    int tc_ok = -1;
+    // tcgen05 fine path
+    bool use_tc = false;
+    int tc_terms = 3;
+    DevBuf<uint32_t> x16h, x16l;
+    DevBuf<unsigned> maxbits;
+    CUtensorMap tm_hi{}, tm_lo{};
 };
 
 namespace {
@@ -440,7 +496,19 @@ void engine_init(ltci_engine* e) {
     e->batch = std::max<unsigned long long>(1, std::min<unsigned long long>(pl.coarse_cells, budget / per_coarse));
     // the fine kernel indexes rows with int
     e->batch = std::min<unsigned long long>(e->batch, (1ull << 30) / std::max(1, pl.R_slice));
-    e->X.ensure(e->batch * per_coarse / sizeof(float2));
+    e->use_tc = tc_fine_selected(pl.fine_path, M, pl.D, pl.keep_dense);
+    e->tc_terms = tc_terms_for(pl.fine_path);
+    if (e->use_tc) {
+        const size_t words = e->batch * static_cast<size_t>(pl.R_slice) * M;  // one half2 per complex sample
+        e->x16h.ensure(words);
+        e->x16l.ensure(words);
+        e->maxbits.ensure(1);
+        const unsigned long long rows_cap = e->batch * static_cast<unsigned long long>(pl.R_slice);
+        e->tm_hi = make_x16_map(e->x16h.p, M, rows_cap);
+        e->tm_lo = make_x16_map(e->x16l.p, M, rows_cap);
+    } else {
+        e->X.ensure(e->batch * per_coarse / sizeof(float2));
+    }
     const unsigned long long H = pl.coarse_cells * pl.fine_cells * pl.R_slice * pl.D;
     e->cand_cap = std::max<unsigned long long>(1, std::min<unsigned long long>(H, 1ull << 22));
     e->cand.ensure(e->cand_cap);
@@ -545,7 +613,33 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
         fa.retain2 = pl.retain < 0 ? -1.0f : static_cast<float>(r2);
     }
 
-    const bool use_tc = tc_fine_selected(pl.fine_path, M, pl.D, pl.keep_dense);
+    const bool use_tc = e->use_tc;
+    TcArgs ta{};
+    if (use_tc) {
+        ca.Xh = e->x16h.p;
+        ca.Xl = e->x16l.p;
+        ca.maxbits = e->maxbits.p;
+        CK(cudaMemsetAsync(e->maxbits.p, 0, sizeof(unsigned), st));
+        const size_t n = static_cast<size_t>(K) * M;
+        cube_maxabs_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, st>>>(input, n,
+                                                                                                        e->maxbits.p);
+        CK(cudaGetLastError());
+        ++e->launches;
+        ta.f = fa;
+        ta.M = M;
+        ta.K = K;
+        ta.nfa = static_cast<int>(pl.fine_axes.size());
+        for (int i = 0; i < ta.nfa && i < 3; ++i) {
+            ta.fcount[i] = pl.fine_axes[i].count;
+            ta.fstart[i] = pl.fine_axes[i].start;
+            ta.fstep[i] = pl.fine_axes[i].step;
+            ta.ford[i] = pl.fine_orders[i];
+        }
+        ta.coef_cycles = 2.0 * pl.kappa / lambda_of(pl.rp);
+        ta.inv_prf = 1.0 / pl.rp.PRF;
+        ta.tab_f = static_cast<int>(std::min<unsigned long long>(pl.fine_cells, (TC_QT - 1) / pl.D + 2));
+        ta.maxbits = e->maxbits.p;
+    }
     for (unsigned long long c0 = 0; c0 < pl.coarse_cells; c0 += e->batch) {
         const unsigned long long cc = std::min<unsigned long long>(e->batch, pl.coarse_cells - c0);
         ca.c_begin = c0;
@@ -556,14 +650,20 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
             evi += 4;
             CK(cudaEventRecord(e->ev[evc], st));
         }
-        launch_coarse(ca, pg, st);
+        launch_coarse(ca, pg, st, use_tc);
         ++e->launches;
         if (evc >= 0) CK(cudaEventRecord(e->ev[evc + 1], st));
         fa.c_begin = c0;
         fa.rows = static_cast<int>(cc) * pl.R_slice;
         if (evc >= 0) CK(cudaEventRecord(e->ev[evc + 2], st));
         if (use_tc) {
-            e->launches += tc_fine_launch(fa, M, st);
+            ta.f.c_begin = c0;
+            ta.f.rows = fa.rows;
+            if (e->tc_terms == 1)
+                launch_tc_terms<1>(ta, e->tm_hi, e->tm_lo, st);
+            else
+                launch_tc_terms<3>(ta, e->tm_hi, e->tm_lo, st);
+            ++e->launches;
         } else {
             if (pl.keep_dense)
                 launch_fine_m<true>(fa, M, st);

@@ -1,21 +1,435 @@
-// fine_tc.cuh -- K2a: fine stage as a dense complex contraction on tcgen05
-// tensor cores.  Selection helper + launcher.
+// fine_tc.cuh -- K2a: the fine Doppler-frequency-migration stage as a dense
+// complex contraction on the 5th-generation tensor cores (tcgen05 + TMEM +
+// TMA), fused with the K3 statistic reduction.
+//
+// For a batch of coarse-compensated rows X[rho, m] (rho = (coarse cell,
+// range cell)) the fine stage of the reference (gft over the Doppler window,
+// proj/src/transforms.cpp:180-214, scanned by UnitScan, detectors.cpp:23-31)
+// is
+//     Y[rho, q] = sum_m X[rho, m] * B[m, q],   q = f*D + jj,
+//     B[m, q]   = H_f(m) * w_M^{d m},  d = dop_first + jj - M/2,
+// (pre-recentring convention, like the FFT path: the unit-modulus factor
+// e^{j 2 pi d/M} is applied on the host to returned values).  B does not
+// depend on the coarse cell, so the whole stage is one GEMM.
+//
+// Real-ified with complex interleaving along K (k' = 2m + {re, im}):
+//   A operand (MMA M = 128): generated steering tile, row n' = 2q + part,
+//        part 0 -> (Br, -Bi), part 1 -> (Bi, Br) at (k' = 2m, 2m + 1);
+//   B operand (MMA N = 256): X rows, K-major fp16, loaded by TMA (SW128);
+//   D (TMEM, fp32, 128 lanes x 256 columns): Re Y at even lanes, Im Y at odd.
+// Split precision: x = x_hi + x_lo in fp16 (global power-of-two prescale s
+// keeps X in fp16's normal range); TERMS = 3 accumulates A_hi X_hi + A_lo X_hi
+// + A_hi X_lo (error ~1e-7 rel., FP32 class); TERMS = 1 is A_hi X_hi (~3e-4 of
+// the row maximum, inside the 1e-3 contract; opt-in).
+//
+// Warp roles (192 threads, one CTA per (64 complex outputs) x (256 rows) tile):
+//   warp 0     TMEM allocation; one lane issues the TMA loads of X tiles
+//   warp 1     one lane issues tcgen05.mma and tcgen05.commit
+//   warps 2-5  generate the steering tile in swizzled smem from per-CTA
+//              tables (H_f(m) evaluated in FP64 cycles, w_M^k exact-index
+//              table), then run the epilogue: tcgen05.ld, |Y|^2, threshold
+//              compaction, per-row argmax (redux.sync + ballot, ties to the
+//              lowest q), one 128-bit CAS per row into the per-cell peak slot.
 #pragma once
 
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include "coarse.cuh"
 #include "fine_fft.cuh"
 
 namespace ltcib {
 
-// AUTO keeps the CUDA-core FFT path until the tensor path is built.
-inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
-    (void)M;
-    (void)D;
-    (void)keep_dense;
-    if (fine_path == 2 /* LTCI_FINE_TC_DENSE */)
-        throw std::runtime_error("ltci_cuda: tcgen05 fine path not available in this build");
-    return false;
+constexpr int TC_BM = 128;    // real output columns per tile (MMA M)
+constexpr int TC_BN = 256;    // X rows per tile (MMA N)
+constexpr int TC_BK = 64;     // real K per k-block: 128-byte rows, SW128
+constexpr int TC_QT = TC_BM / 2;
+constexpr int TC_THREADS = 192;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
+constexpr int TC_X_BYTES = TC_BN * TC_BK * 2;
+
+struct TcArgs {
+    FineArgs f;                 // shared indexing / output fields
+    int M, K;
+    int nfa;                    // fine axes (0..3)
+    int fcount[3], ford[3];
+    double fstart[3], fstep[3];
+    double coef_cycles;         // 2 kappa / lambda
+    double inv_prf;
+    int tab_f;                  // H-table capacity in fine cells
+    const unsigned* maxbits;    // max |y|^2 of the coarse-stage input (float bits)
+};
+
+// ------------------------------------------------------------- PTX glue ---
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-inline int tc_fine_launch(const FineArgs&, int, cudaStream_t) { return 0; }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
+    const long long t0 = clock64();
+#pragma unroll 1
+    for (;;) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > 20000000000ll) __trap();  // ~10 s: protocol bug, fail the launch
+    }
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (!done) mbar_wait_slow(bar, parity);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128-byte swizzle, 8-row core groups 1024 B apart (SBO), sm100 version bit.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;             // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;     // SBO
+    d |= static_cast<uint64_t>(1) << 46;             // descriptor version (Blackwell)
+    d |= static_cast<uint64_t>(2) << 61;             // SWIZZLE_128B
+    return d;
+}
+
+// kind::f16 instruction descriptor: F32 accumulate, F16 A/B, both K-major.
+__host__ __device__ constexpr uint32_t tc_idesc(int m, int n) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float2 unpack_half2(uint32_t u) {
+    __half2 h = *reinterpret_cast<__half2*>(&u);
+    return __half22float2(h);
+}
+
+template <int TERMS>
+__host__ __device__ constexpr int tc_stages() {
+    return TERMS == 3 ? 2 : 4;
+}
+
+template <int TERMS>
+__host__ __device__ constexpr int tc_stage_bytes() {
+    return (TERMS == 3 ? 2 : 1) * (TC_A_BYTES + TC_X_BYTES);
+}
+
+// ------------------------------------------------------------- kernel -----
+template <int TERMS>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    fine_tc_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ CUtensorMap tm_hi,
+                   const __grid_constant__ CUtensorMap tm_lo) {
+    constexpr int STAGES = tc_stages<TERMS>();
+    constexpr int PLANES = TERMS == 3 ? 2 : 1;
+    constexpr int SB = tc_stage_bytes<TERMS>();
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const FineArgs& fa = a.f;
+    const int M = a.M;
+    float2* s_H = reinterpret_cast<float2*>(smem + STAGES * SB);      // [tab_f][M]
+    float2* s_W = s_H + static_cast<size_t>(a.tab_f) * M;                // [M]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_W + M);               // full, empty, tmem_full
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+    // [4][TC_BN] (key, lane, re, im): aliases the stage buffers, which are
+    // drained once the last MMA has committed (epilogue only).
+    uint4* s_best = reinterpret_cast<uint4*>(smem);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q0 = blockIdx.x * TC_QT;
+    const int row0 = blockIdx.y * TC_BN;
+    const int Q = static_cast<int>(fa.F) * fa.D;
+    const int nkb = (2 * M) / TC_BK;
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES), tfull = smem_u32(bars + 2 * STAGES);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1 + 4);  // TMA producer + 4 generator warps
+            mbar_init(empty0 + 8 * s, 1);     // tcgen05.commit
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                     "r"(TC_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    const int f_lo = q0 / fa.D;
+    const int f_hi = min(static_cast<int>(fa.F) - 1, (q0 + TC_QT - 1) / fa.D);
+    if (warp >= 2) {
+        // per-CTA tables: H_f(m) for this tile's fine cells (FP64 cycles), w_M^k
+        const int gt = threadIdx.x - 64;
+        const int nf = f_hi - f_lo + 1;
+        for (int i = gt; i < nf * M; i += 128) {
+            const int fl = i / M, m = i - fl * M;
+            int rem = f_lo + fl;
+            const double t = static_cast<double>(m + 1) * a.inv_prf;
+            double cyc = 0.0;
+            for (int ax = a.nfa - 1; ax >= 0; --ax) {
+                const int idx = rem % a.fcount[ax];
+                rem /= a.fcount[ax];
+                double tp = 1.0;
+                for (int p = 0; p < a.ford[ax]; ++p) tp *= t;
+                cyc += a.coef_cycles * (a.fstart[ax] + a.fstep[ax] * idx) * tp;
+            }
+            const double fr = cyc - rint(cyc);
+            float s, c;
+            sincospif(static_cast<float>(2.0 * fr), &s, &c);
+            s_H[i] = make_float2(c, s);
+        }
+        for (int k = gt; k < M; k += 128) {
+            float s, c;
+            sincospif(2.0f * static_cast<float>(k) / static_cast<float>(M), &s, &c);
+            s_W[k] = make_float2(c, s);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *s_tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(empty0 + 8 * s, ph ^ 1);
+                uint8_t* st = smem + s * SB;
+                mbar_expect_tx(full0 + 8 * s, PLANES * TC_X_BYTES);
+                tma_load_2d(smem_u32(st), &tm_hi, kb * TC_BK, row0, full0 + 8 * s);
+                if (TERMS == 3) tma_load_2d(smem_u32(st + TC_X_BYTES), &tm_lo, kb * TC_BK, row0, full0 + 8 * s);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc_idesc(TC_BM, TC_BN);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(full0 + 8 * s, ph);
+                tc_fence_after();
+                const uint32_t st = smem_u32(smem + s * SB);
+                const uint32_t x_hi = st, x_lo = st + TC_X_BYTES;
+                const uint32_t a_hi = st + PLANES * TC_X_BYTES, a_lo = a_hi + TC_A_BYTES;
+#pragma unroll
+                for (int ks = 0; ks < TC_BK / 16; ++ks) {
+                    const uint32_t off = ks * 32;  // 16 fp16 along K
+                    tc_mma(tmem, sw128_desc(a_hi + off), sw128_desc(x_hi + off), idesc, (kb | ks) != 0);
+                    if (TERMS == 3) {
+                        tc_mma(tmem, sw128_desc(a_lo + off), sw128_desc(x_hi + off), idesc, 1);
+                        tc_mma(tmem, sw128_desc(a_hi + off), sw128_desc(x_lo + off), idesc, 1);
+                    }
+                }
+                tc_commit(empty0 + 8 * s);
+            }
+            tc_commit(tfull);
+        }
+    } else {
+        // ---------------- generators (A operand) ----------------
+        const int quad = warp & 3;             // TMEM lane quadrant of this warp
+        const int L = 32 * quad + lane;        // A row = TMEM lane = real output column
+        const int qc = q0 + (L >> 1);
+        const int part = L & 1;
+        const bool qvalid = qc < Q;
+        const int f = qvalid ? qc / fa.D : f_lo;
+        const int jj = qvalid ? qc - f * fa.D : 0;
+        const int d = jj + fa.dop_first - M / 2;
+        const float2* Hrow = s_H + static_cast<size_t>(f - f_lo) * M;
+        const int rsw = L & 7;
+        const uint32_t row_off = (L >> 3) * 1024 + rsw * 128;
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
+            mbar_wait(empty0 + 8 * s, ph ^ 1);
+            uint8_t* a_hi = smem + s * SB + PLANES * TC_X_BYTES;
+            uint8_t* a_lo = a_hi + TC_A_BYTES;
+            const int m0 = kb * (TC_BK / 2);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int m = m0 + 4 * c + e;
+                    const float2 h = Hrow[m];
+                    const float2 w = s_W[(d * m) & (M - 1)];
+                    float2 b = cmul(h, w);
+                    if (!qvalid) b = make_float2(0.f, 0.f);
+                    const float p0 = part ? b.y : b.x;
+                    const float p1 = part ? b.x : -b.y;
+                    hi[e] = pack_half2(p0, p1);
+                    if (TERMS == 3) {
+                        const float2 hf = unpack_half2(hi[e]);
+                        lo[e] = pack_half2(p0 - hf.x, p1 - hf.y);
+                    }
+                }
+                const uint32_t chunk = row_off + ((c ^ rsw) << 4);
+                *reinterpret_cast<uint4*>(a_hi + chunk) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                if (TERMS == 3) *reinterpret_cast<uint4*>(a_lo + chunk) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full0 + 8 * s);
+        }
+
+        // ---------------- epilogue ----------------
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        const float inv_s = 1.0f / fp16_prescale(a.maxbits, a.K);
+        for (int cb = 0; cb < TC_BN / 32; ++cb) {
+            uint32_t r[32];
+            tmem_ld32(tmem + (static_cast<uint32_t>(32 * quad) << 16) + cb * 32, r);
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+                const int col = cb * 32 + j;
+                const int rho = row0 + col;
+                const float v = __uint_as_float(r[j]) * inv_s;
+                const float pv = __shfl_xor_sync(0xffffffffu, v, 1);
+                const float re = part ? pv : v, im = part ? v : pv;
+                const bool ok = qvalid && part == 0 && rho < fa.rows;
+                const float m2 = ok ? mag2f(re, im) : -1.f;
+                if (ok && (fa.dense != nullptr || m2 > fa.retain2)) {
+                    const int c_local = rho / fa.R_slice;
+                    emit_cell(fa, make_float2(re, im), m2, static_cast<unsigned>(f), jj,
+                              fa.c_begin + c_local, fa.row_begin + (rho - c_local * fa.R_slice),
+                              fa.dense != nullptr);
+                }
+                const unsigned key = m2 >= 0.f ? __float_as_uint(m2) + 1u : 0u;
+                const unsigned mx = __reduce_max_sync(0xffffffffu, key);
+                const unsigned bal = __ballot_sync(0xffffffffu, key == mx && mx != 0u);
+                const int wl = bal ? __ffs(bal) - 1 : 0;
+                const float bre = __shfl_sync(0xffffffffu, re, wl);
+                const float bim = __shfl_sync(0xffffffffu, im, wl);
+                if (lane == 0)
+                    s_best[quad * TC_BN + col] = make_uint4(mx, static_cast<unsigned>(32 * quad + wl),
+                                                            __float_as_uint(bre), __float_as_uint(bim));
+            }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int col = threadIdx.x - 64; col < TC_BN; col += 128) {
+            const int rho = row0 + col;
+            if (rho >= fa.rows) continue;
+            uint4 b = s_best[col];
+            for (int qd = 1; qd < 4; ++qd) {
+                const uint4 o = s_best[qd * TC_BN + col];
+                if (o.x > b.x) b = o;  // strictly greater: lower quadrant (lower q) wins ties
+            }
+            if (b.x == 0u) continue;
+            const int qb = q0 + static_cast<int>(b.y >> 1);
+            const int fb = qb / fa.D, jb = qb - fb * fa.D;
+            const int c_local = rho / fa.R_slice;
+            const int r_local = rho - c_local * fa.R_slice;
+            const unsigned long long flat =
+                (((fa.c_begin + c_local) * fa.F + fb) * fa.R_total + static_cast<unsigned long long>(fa.row_begin + r_local)) *
+                    fa.D + jb;
+            peak_publish(fa.slots + r_local, __uint_as_float(b.z), __uint_as_float(b.w), flat);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_BN));
+    }
+}
+
+// Max |y|^2 over the coarse-stage input (for the fp16 prescale).
+__global__ void cube_maxabs_kernel(const float2* __restrict__ y, size_t n, unsigned* maxbits) {
+    float m = 0.f;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        m = fmaxf(m, mag2f(y[i].x, y[i].y));
+    unsigned u = __float_as_uint(m);
+    u = __reduce_max_sync(0xffffffffu, u);
+    if ((threadIdx.x & 31) == 0) atomicMax(maxbits, u);
+}
+
+// ------------------------------------------------------------- host -------
+inline int tc_terms_for(int fine_path) { return fine_path == 3 /* LTCI_FINE_TC_FAST */ ? 1 : 3; }
+
+inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
+    (void)D;
+    (void)keep_dense;
+    if (fine_path == 2 || fine_path == 3) {
+        if (M < 32) throw std::invalid_argument("ltci_cuda: tcgen05 fine path needs M >= 32");
+        return true;
+    }
+    return false;  // AUTO: CUDA-core FFT path (see DESIGN.md for the per-shape choice)
+}
+
+inline size_t tc_smem_bytes(int terms, int tab_f, int M) {
+    const size_t stages = terms == 3 ? static_cast<size_t>(tc_stages<3>()) * tc_stage_bytes<3>()
+                                     : static_cast<size_t>(tc_stages<1>()) * tc_stage_bytes<1>();
+    return 1024 + stages + (static_cast<size_t>(tab_f) + 1) * M * sizeof(float2) + 8 * (2 * 4 + 1) + 16;
+}
 
 }  // namespace ltcib
