@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--fine-path", default="auto", choices=["auto", "fft", "tc"])
+    ap.add_argument("--fine-path", default="auto", choices=["auto", "fft", "tc", "tcfast"])
     ap.add_argument("--pfa", type=float, default=1e-6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample length")
@@ -205,7 +205,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     p, s = w.params, w.space
-    fine_path = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE}[args.fine_path]
+    fine_path = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE,
+                 "tcfast": A.FINE_TC_FAST}[args.fine_path]
     gamma = detection_threshold(p, w.sigma2, args.pfa)
     opt = DetectorOptions(retain_threshold=gamma, fine_path=fine_path, device=local)
     R = s.roi.count()

@@ -13,13 +13,13 @@ from paper_2403_06788_b200.model import DetectorOptions  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--runs", type=int, default=1)
-ap.add_argument("--fine-path", default="auto", choices=["auto", "fft", "tc"])
+ap.add_argument("--fine-path", default="auto", choices=["auto", "fft", "tc", "tcfast"])
 ap.add_argument("--coarse-v", type=int, default=0, help="slice the coarse velocity axis")
 a = ap.parse_args()
 w = configs.config(a.config)
 if a.coarse_v:
     w = configs.sliced(w, a.coarse_v)
-fp = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE}[a.fine_path]
+fp = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE, "tcfast": A.FINE_TC_FAST}[a.fine_path]
 opt = DetectorOptions(retain_threshold=detection_threshold(w.params, w.sigma2, 1e-6), fine_path=fp)
 e = Engine(w.params, w.space, w.variant, w.amb, opt)
 x = scene.to_complex64_roundtrip(w.cube())
