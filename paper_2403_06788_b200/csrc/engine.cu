@@ -358,12 +358,12 @@ EncodeTiledFn encode_tiled() {
     return fn;
 }
 
-// [rows][2M] fp16, box 64 (K) x 256 (rows), 128-byte swizzle (matches sw128_desc)
+// [rows][2M] fp16, box 64 (K) x 128 (rows), 128-byte swizzle (matches sw128_desc)
 CUtensorMap make_x16_map(void* base, int M, unsigned long long rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * M), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * M) * 2};
-    const cuuint32_t box[2] = {TC_BK, TC_BN};
+    const cuuint32_t box[2] = {TC_BK, TC_BM};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, estr,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -375,11 +375,15 @@ CUtensorMap make_x16_map(void* base, int M, unsigned long long rows) {
 template <int TERMS>
 void launch_tc_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& lo, cudaStream_t st) {
     auto kern = fine_tc_kernel<TERMS>;
-    const size_t smem = tc_smem_bytes(TERMS, a.tab_f, a.M);
-    if (smem > 227 * 1024) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: tcgen05 tile tables exceed shared memory");
+    const size_t smem = tc_smem_bytes(TERMS, a.M);
+    if (smem > 227 * 1024) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: tcgen05 tiles exceed shared memory");
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const int Q = static_cast<int>(a.f.F) * a.f.D;
-    dim3 grid((Q + TC_QT - 1) / TC_QT, (a.f.rows + TC_BN - 1) / TC_BN);
+    const long long Q = static_cast<long long>(a.f.F) * a.f.D;
+    const long long tiles = ((Q + TC_QT - 1) / TC_QT) * ((a.f.rows + TC_BM - 1) / TC_BM);
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = static_cast<int>(std::min<long long>(tiles, sms));  // persistent: one CTA per SM
     kern<<<grid, TC_THREADS, smem, st>>>(a, hi, lo);
     CK(cudaGetLastError());
 }
@@ -459,6 +463,8 @@ struct ltci_engine {
     int tc_terms = 3;
     DevBuf<uint32_t> x16h, x16l;
     DevBuf<unsigned> maxbits;
+    DevBuf<float2> htab;
+    bool htab_ready = false;
     CUtensorMap tm_hi{}, tm_lo{};
 };
 
@@ -637,8 +643,18 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
         }
         ta.coef_cycles = 2.0 * pl.kappa / lambda_of(pl.rp);
         ta.inv_prf = 1.0 / pl.rp.PRF;
-        ta.tab_f = static_cast<int>(std::min<unsigned long long>(pl.fine_cells, (TC_QT - 1) / pl.D + 2));
         ta.maxbits = e->maxbits.p;
+        if (!e->htab_ready) {
+            // H_f(m) for every fine cell, FP64 phases, built once per engine
+            e->htab.ensure(static_cast<size_t>(pl.fine_cells) * M);
+            const size_t total = static_cast<size_t>(pl.fine_cells) * M;
+            build_htab_kernel<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(
+                ta, e->htab.p);
+            CK(cudaGetLastError());
+            ++e->launches;
+            e->htab_ready = true;
+        }
+        ta.htab = e->htab.p;
     }
     for (unsigned long long c0 = 0; c0 < pl.coarse_cells; c0 += e->batch) {
         const unsigned long long cc = std::min<unsigned long long>(e->batch, pl.coarse_cells - c0);

@@ -40,13 +40,15 @@
 
 namespace ltcib {
 
-constexpr int TC_BM = 128;    // real output columns per tile (MMA M)
-constexpr int TC_BN = 256;    // X rows per tile (MMA N)
+constexpr int TC_BM = 128;    // X rows per tile (MMA M)
+constexpr int TC_BN = 256;    // real output columns per tile (MMA N) = 128 complex outputs
 constexpr int TC_BK = 64;     // real K per k-block: 128-byte rows, SW128
-constexpr int TC_QT = TC_BM / 2;
-constexpr int TC_THREADS = 320;  // 2 control warps + 8 generator/epilogue warps
-constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
-constexpr int TC_X_BYTES = TC_BN * TC_BK * 2;
+constexpr int TC_QT = TC_BN / 2;
+constexpr int TC_GEN_WARPS = 8;
+constexpr int TC_EPI_WARPS = 4;
+constexpr int TC_THREADS = 32 * (2 + TC_GEN_WARPS + TC_EPI_WARPS);
+constexpr int TC_X_BYTES = TC_BM * TC_BK * 2;
+constexpr int TC_G_BYTES = TC_BN * TC_BK * 2;
 
 struct TcArgs {
     FineArgs f;                 // shared indexing / output fields
@@ -56,7 +58,7 @@ struct TcArgs {
     double fstart[3], fstep[3];
     double coef_cycles;         // 2 kappa / lambda
     double inv_prf;
-    int tab_f;                  // H-table capacity in fine cells
+    const float2* htab;         // [F][M] H_f(m), built by build_htab_kernel
     const unsigned* maxbits;    // max |y|^2 of the coarse-stage input (float bits)
 };
 
@@ -181,10 +183,14 @@ __host__ __device__ constexpr int tc_stages() {
 
 template <int TERMS>
 __host__ __device__ constexpr int tc_stage_bytes() {
-    return (TERMS == 3 ? 2 : 1) * (TC_A_BYTES + TC_X_BYTES);
+    return (TERMS == 3 ? 2 : 1) * (TC_X_BYTES + TC_G_BYTES);
 }
 
 // ------------------------------------------------------------- kernel -----
+// Persistent: each CTA walks tiles t = blockIdx.x, + gridDim.x, ...; tile t =
+// (row tile t / nq, q tile t % nq), q fastest so co-resident CTAs share the
+// X row tile in L2.  TMEM holds two 128 x 256 fp32 accumulators so the
+// epilogue of tile i overlaps the MMAs of tile i + 1.
 template <int TERMS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fine_tc_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ CUtensorMap tm_hi,
@@ -192,66 +198,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int STAGES = tc_stages<TERMS>();
     constexpr int PLANES = TERMS == 3 ? 2 : 1;
     constexpr int SB = tc_stage_bytes<TERMS>();
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment by offsetting the shared array itself, so every
+    // derived pointer stays in the shared state space (LDS/STS, not LD/ST).
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const FineArgs& fa = a.f;
     const int M = a.M;
-    float2* s_H = reinterpret_cast<float2*>(smem + STAGES * SB);      // [tab_f][M]
-    float2* s_W = s_H + static_cast<size_t>(a.tab_f) * M;                // [M]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_W + M);               // full, empty, tmem_full
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
-    // [4][TC_BN] (key, lane, re, im): aliases the stage buffers, which are
-    // drained once the last MMA has committed (epilogue only).
-    uint4* s_best = reinterpret_cast<uint4*>(smem);
+    float2* s_W = reinterpret_cast<float2*>(smem + STAGES * SB);         // [M]  w_M^k
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_W + M);
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q0 = blockIdx.x * TC_QT;
-    const int row0 = blockIdx.y * TC_BN;
     const int Q = static_cast<int>(fa.F) * fa.D;
+    const int nq = (Q + TC_QT - 1) / TC_QT;
+    const int nrt = (fa.rows + TC_BM - 1) / TC_BM;
+    const int ntiles = nq * nrt;
     const int nkb = (2 * M) / TC_BK;
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES), tfull = smem_u32(bars + 2 * STAGES);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+    const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(full0 + 8 * s, 1 + 8);  // TMA producer + 8 generator warps
-            mbar_init(empty0 + 8 * s, 1);     // tcgen05.commit
+            mbar_init(full0 + 8 * s, 1 + TC_GEN_WARPS);  // TMA producer + generator warps
+            mbar_init(empty0 + 8 * s, 1);                 // tcgen05.commit
         }
-        mbar_init(tfull, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);                 // tcgen05.commit after a tile's last k-block
+            mbar_init(tempty0 + 8 * b, TC_EPI_WARPS);     // epilogue warps drained the accumulator
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
-                     "r"(TC_BN));
+                     "r"(2 * TC_BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    const int f_lo = q0 / fa.D;
-    const int f_hi = min(static_cast<int>(fa.F) - 1, (q0 + TC_QT - 1) / fa.D);
-    if (warp >= 2) {
-        // per-CTA tables: H_f(m) for this tile's fine cells (FP64 cycles), w_M^k
-        const int gt = threadIdx.x - 64;
-        const int nf = f_hi - f_lo + 1;
-        for (int i = gt; i < nf * M; i += 256) {
-            const int fl = i / M, m = i - fl * M;
-            int rem = f_lo + fl;
-            const double t = static_cast<double>(m + 1) * a.inv_prf;
-            double cyc = 0.0;
-            for (int ax = a.nfa - 1; ax >= 0; --ax) {
-                const int idx = rem % a.fcount[ax];
-                rem /= a.fcount[ax];
-                double tp = 1.0;
-                for (int p = 0; p < a.ford[ax]; ++p) tp *= t;
-                cyc += a.coef_cycles * (a.fstart[ax] + a.fstep[ax] * idx) * tp;
-            }
-            const double fr = cyc - rint(cyc);
-            float s, c;
-            sincospif(static_cast<float>(2.0 * fr), &s, &c);
-            s_H[i] = make_float2(c, s);
-        }
-        for (int k = gt; k < M; k += 256) {
-            float s, c;
-            sincospif(2.0f * static_cast<float>(k) / static_cast<float>(M), &s, &c);
-            s_W[k] = make_float2(c, s);
-        }
+    for (int k = threadIdx.x; k < M; k += TC_THREADS) {
+        float s, c;
+        sincospif(2.0f * static_cast<float>(k) / static_cast<float>(M), &s, &c);
+        s_W[k] = make_float2(c, s);
     }
     tc_fence_before();
     __syncthreads();
@@ -259,160 +244,178 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t tmem = *s_tmem;
 
     if (warp == 0) {
+        // ---------------- TMA producer: X tiles (MMA A operand) ----------------
         if (lane == 0) {
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(empty0 + 8 * s, ph ^ 1);
-                uint8_t* st = smem + s * SB;
-                mbar_expect_tx(full0 + 8 * s, PLANES * TC_X_BYTES);
-                tma_load_2d(smem_u32(st), &tm_hi, kb * TC_BK, row0, full0 + 8 * s);
-                if (TERMS == 3) tma_load_2d(smem_u32(st + TC_X_BYTES), &tm_lo, kb * TC_BK, row0, full0 + 8 * s);
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int row0 = (t / nq) * TC_BM;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(empty0 + 8 * s, ph ^ 1);
+                    uint8_t* st = smem + s * SB;
+                    mbar_expect_tx(full0 + 8 * s, PLANES * TC_X_BYTES);
+                    tma_load_2d(smem_u32(st), &tm_hi, kb * TC_BK, row0, full0 + 8 * s);
+                    if (TERMS == 3) tma_load_2d(smem_u32(st + TC_X_BYTES), &tm_lo, kb * TC_BK, row0, full0 + 8 * s);
+                }
             }
         }
     } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
         if (lane == 0) {
             constexpr uint32_t idesc = tc_idesc(TC_BM, TC_BN);
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(full0 + 8 * s, ph);
+            int it = 0, i = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const int ab = i & 1;
+                mbar_wait(tempty0 + 8 * ab, ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t st = smem_u32(smem + s * SB);
-                const uint32_t x_hi = st, x_lo = st + TC_X_BYTES;
-                const uint32_t a_hi = st + PLANES * TC_X_BYTES, a_lo = a_hi + TC_A_BYTES;
+                const uint32_t dcol = tmem + ab * TC_BN;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(full0 + 8 * s, ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * SB);
+                    const uint32_t x_hi = st, x_lo = st + TC_X_BYTES;
+                    const uint32_t g_hi = st + PLANES * TC_X_BYTES, g_lo = g_hi + TC_G_BYTES;
 #pragma unroll
-                for (int ks = 0; ks < TC_BK / 16; ++ks) {
-                    const uint32_t off = ks * 32;  // 16 fp16 along K
-                    tc_mma(tmem, sw128_desc(a_hi + off), sw128_desc(x_hi + off), idesc, (kb | ks) != 0);
-                    if (TERMS == 3) {
-                        tc_mma(tmem, sw128_desc(a_lo + off), sw128_desc(x_hi + off), idesc, 1);
-                        tc_mma(tmem, sw128_desc(a_hi + off), sw128_desc(x_lo + off), idesc, 1);
+                    for (int ks = 0; ks < TC_BK / 16; ++ks) {
+                        const uint32_t off = ks * 32;  // 16 fp16 along K
+                        tc_mma(dcol, sw128_desc(x_hi + off), sw128_desc(g_hi + off), idesc, (kb | ks) != 0);
+                        if (TERMS == 3) {
+                            tc_mma(dcol, sw128_desc(x_hi + off), sw128_desc(g_lo + off), idesc, 1);
+                            tc_mma(dcol, sw128_desc(x_lo + off), sw128_desc(g_hi + off), idesc, 1);
+                        }
+                    }
+                    tc_commit(empty0 + 8 * s);
+                }
+                tc_commit(tfull0 + 8 * ab);
+            }
+        }
+    } else if (warp < 2 + TC_GEN_WARPS) {
+        // ---------------- steering generators (MMA B operand) ----------------
+        // thread -> (q_local, 16-byte chunk) items; every complex steering value
+        // is computed once and written to both of its real rows
+        // (2q: (Br, -Bi) -> Re Y, 2q+1: (Bi, Br) -> Im Y).
+        const int gt = threadIdx.x - 64;              // 0..255
+        const int qa = (gt & 7) + 8 * (gt >> 5);      // 0..63, second item at qa + 64
+        const int c_base = (gt >> 3) & 3;             // chunks c_base, c_base + 4
+        int it = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int q0 = (t % nq) * TC_QT;
+            int dq[2];
+            const float2* Hq[2];
+            bool vq[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int qc = q0 + qa + 64 * u;
+                vq[u] = qc < Q;
+                const int f = vq[u] ? qc / fa.D : 0;
+                const int jj = vq[u] ? qc - f * fa.D : 0;
+                dq[u] = jj + fa.dop_first - M / 2;
+                Hq[u] = a.htab + static_cast<size_t>(f) * M;
+            }
+            for (int kb = 0; kb < nkb; ++kb, ++it) {
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                mbar_wait(empty0 + 8 * s, ph ^ 1);
+                uint8_t* g_hi = smem + s * SB + PLANES * TC_X_BYTES;
+                uint8_t* g_lo = g_hi + TC_G_BYTES;
+                const int m0 = kb * (TC_BK / 2);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int L0 = 2 * (qa + 64 * u), L1 = L0 + 1;
+                    const uint32_t r0 = (L0 >> 3) * 1024 + (L0 & 7) * 128;
+                    const uint32_t r1 = (L1 >> 3) * 1024 + (L1 & 7) * 128;
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int c = c_base + 4 * hh;
+                        uint32_t h0[4], h1[4], l0[4], l1[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int m = m0 + 4 * c + e;
+                            float2 b = cmul(__ldg(Hq[u] + m), s_W[(dq[u] * m) & (M - 1)]);
+                            if (!vq[u]) b = make_float2(0.f, 0.f);
+                            const uint32_t hb = pack_half2(b.x, b.y);     // (Br, Bi) hi
+                            h0[e] = hb ^ 0x80000000u;                     // (Br, -Bi)
+                            h1[e] = __byte_perm(hb, 0, 0x1032);           // (Bi, Br)
+                            if (TERMS == 3) {
+                                const float2 hf = unpack_half2(hb);
+                                const uint32_t lb = pack_half2(b.x - hf.x, b.y - hf.y);
+                                l0[e] = lb ^ 0x80000000u;
+                                l1[e] = __byte_perm(lb, 0, 0x1032);
+                            }
+                        }
+                        const uint32_t o0 = r0 + ((c ^ (L0 & 7)) << 4);
+                        const uint32_t o1 = r1 + ((c ^ (L1 & 7)) << 4);
+                        *reinterpret_cast<uint4*>(g_hi + o0) = make_uint4(h0[0], h0[1], h0[2], h0[3]);
+                        *reinterpret_cast<uint4*>(g_hi + o1) = make_uint4(h1[0], h1[1], h1[2], h1[3]);
+                        if (TERMS == 3) {
+                            *reinterpret_cast<uint4*>(g_lo + o0) = make_uint4(l0[0], l0[1], l0[2], l0[3]);
+                            *reinterpret_cast<uint4*>(g_lo + o1) = make_uint4(l1[0], l1[1], l1[2], l1[3]);
+                        }
                     }
                 }
-                tc_commit(empty0 + 8 * s);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full0 + 8 * s);
             }
-            tc_commit(tfull);
         }
     } else {
-        // ---------------- generators (A operand) ----------------
-        // 8 warps; thread -> (q_local, 16-byte chunk) items; each complex
-        // steering value is computed once and written to both of its real
-        // rows (2q: (Br, -Bi), 2q+1: (Bi, Br)) via sign flip / half swap.
-        const int gt = threadIdx.x - 64;                     // 0..255
-        const int ql = (gt & 7) + 8 * (gt >> 5);             // 0..63
-        const int c_base = (gt >> 3) & 3;                    // chunks c_base, c_base + 4
-        const int qc = q0 + ql;
-        const bool qvalid = qc < Q;
-        const int f = qvalid ? qc / fa.D : f_lo;
-        const int jj = qvalid ? qc - f * fa.D : 0;
-        const int d = jj + fa.dop_first - M / 2;
-        const float2* Hrow = s_H + static_cast<size_t>(f - f_lo) * M;
-        const int L0 = 2 * ql, L1 = 2 * ql + 1;
-        const uint32_t row0_off = (L0 >> 3) * 1024 + (L0 & 7) * 128;
-        const uint32_t row1_off = (L1 >> 3) * 1024 + (L1 & 7) * 128;
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % STAGES;
-            const uint32_t ph = (kb / STAGES) & 1;
-            mbar_wait(empty0 + 8 * s, ph ^ 1);
-            uint8_t* a_hi = smem + s * SB + PLANES * TC_X_BYTES;
-            uint8_t* a_lo = a_hi + TC_A_BYTES;
-            const int m0 = kb * (TC_BK / 2);
+        // ---------------- epilogue: one X row per thread ----------------
+        const int quad = warp & 3;                 // TMEM lane quadrant (warps 10..13 -> 2,3,0,1)
+        const float inv_s = 1.0f / fp16_prescale(a.maxbits, a.K);
+        int i = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int ab = i & 1;
+            const int q0 = (t % nq) * TC_QT;
+            const int rho = (t / nq) * TC_BM + 32 * quad + lane;
+            const bool rvalid = rho < fa.rows;
+            const int c_local = rvalid ? rho / fa.R_slice : 0;
+            const int r_local = rho - c_local * fa.R_slice;
+            const unsigned long long c_glob = fa.c_begin + c_local;
+            const int r_glob = fa.row_begin + r_local;
+            mbar_wait(tfull0 + 8 * ab, (i >> 1) & 1);
+            tc_fence_after();
+            RowBest best{-1.0f, 0xffffffffu, 0.f, 0.f};
+            int qf = q0 / fa.D, qj = q0 - qf * fa.D;    // (f, jj) of the current q, advanced incrementally
+            for (int cb = 0; cb < TC_BN / 32; ++cb) {
+                uint32_t r[32];
+                tmem_ld32(tmem + (static_cast<uint32_t>(32 * quad) << 16) + ab * TC_BN + cb * 32, r);
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int c = c_base + 4 * half;
-                uint32_t h0[4], h1[4], l0[4], l1[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int m = m0 + 4 * c + e;
-                    float2 b = cmul(Hrow[m], s_W[(d * m) & (M - 1)]);
-                    if (!qvalid) b = make_float2(0.f, 0.f);
-                    const uint32_t hb = pack_half2(b.x, b.y);            // (Br, Bi) hi
-                    h0[e] = hb ^ 0x80000000u;                            // (Br, -Bi)
-                    h1[e] = __byte_perm(hb, 0, 0x1032);                  // (Bi, Br)
-                    if (TERMS == 3) {
-                        const float2 hf = unpack_half2(hb);
-                        const uint32_t lb = pack_half2(b.x - hf.x, b.y - hf.y);
-                        l0[e] = lb ^ 0x80000000u;
-                        l1[e] = __byte_perm(lb, 0, 0x1032);
+                for (int j = 0; j < 16; ++j) {
+                    const int q = q0 + cb * 16 + j;
+                    const float re = __uint_as_float(r[2 * j]) * inv_s;
+                    const float im = __uint_as_float(r[2 * j + 1]) * inv_s;
+                    if (rvalid && q < Q) {
+                        const float m2 = mag2f(re, im);
+                        const unsigned lidx = static_cast<unsigned>(q);
+                        if (m2 > best.m) {  // q ascends: strict > keeps the lowest q on ties
+                            best.m = m2;
+                            best.lidx = lidx;
+                            best.re = re;
+                            best.im = im;
+                        }
+                        if (fa.dense != nullptr || m2 > fa.retain2)
+                            emit_cell(fa, make_float2(re, im), m2, static_cast<unsigned>(qf), qj, c_glob, r_glob,
+                                      fa.dense != nullptr);
+                    }
+                    if (++qj == fa.D) {
+                        qj = 0;
+                        ++qf;
                     }
                 }
-                const uint32_t o0 = row0_off + ((c ^ (L0 & 7)) << 4);
-                const uint32_t o1 = row1_off + ((c ^ (L1 & 7)) << 4);
-                *reinterpret_cast<uint4*>(a_hi + o0) = make_uint4(h0[0], h0[1], h0[2], h0[3]);
-                *reinterpret_cast<uint4*>(a_hi + o1) = make_uint4(h1[0], h1[1], h1[2], h1[3]);
-                if (TERMS == 3) {
-                    *reinterpret_cast<uint4*>(a_lo + o0) = make_uint4(l0[0], l0[1], l0[2], l0[3]);
-                    *reinterpret_cast<uint4*>(a_lo + o1) = make_uint4(l1[0], l1[1], l1[2], l1[3]);
-                }
             }
-            fence_proxy_async();
+            // accumulator buffer drained: hand it back to the MMA issuer
+            tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(full0 + 8 * s);
-        }
-
-        // ---------------- epilogue ----------------
-        // warp -> TMEM lane quadrant (warp % 4) and column half ((warp - 2) / 4)
-        const int quad = warp & 3;
-        const int chalf = (warp - 2) >> 2;
-        const int L = 32 * quad + lane;           // real output column of this lane
-        const int eq = q0 + (L >> 1);
-        const int part = L & 1;
-        const bool evalid = eq < Q;
-        const int ef = evalid ? eq / fa.D : 0;
-        const int ejj = evalid ? eq - ef * fa.D : 0;
-        mbar_wait(tfull, 0);
-        tc_fence_after();
-        const float inv_s = 1.0f / fp16_prescale(a.maxbits, a.K);
-        for (int cb = chalf * (TC_BN / 64); cb < (chalf + 1) * (TC_BN / 64); ++cb) {
-            uint32_t r[32];
-            tmem_ld32(tmem + (static_cast<uint32_t>(32 * quad) << 16) + cb * 32, r);
-#pragma unroll 4
-            for (int j = 0; j < 32; ++j) {
-                const int col = cb * 32 + j;
-                const int rho = row0 + col;
-                const float v = __uint_as_float(r[j]) * inv_s;
-                const float pv = __shfl_xor_sync(0xffffffffu, v, 1);
-                const float re = part ? pv : v, im = part ? v : pv;
-                const bool ok = evalid && part == 0 && rho < fa.rows;
-                const float m2 = ok ? mag2f(re, im) : -1.f;
-                if (ok && (fa.dense != nullptr || m2 > fa.retain2)) {
-                    const int c_local = rho / fa.R_slice;
-                    emit_cell(fa, make_float2(re, im), m2, static_cast<unsigned>(ef), ejj,
-                              fa.c_begin + c_local, fa.row_begin + (rho - c_local * fa.R_slice),
-                              fa.dense != nullptr);
-                }
-                const unsigned key = m2 >= 0.f ? __float_as_uint(m2) + 1u : 0u;
-                const unsigned mx = __reduce_max_sync(0xffffffffu, key);
-                const unsigned bal = __ballot_sync(0xffffffffu, key == mx && mx != 0u);
-                const int wl = bal ? __ffs(bal) - 1 : 0;
-                const float bre = __shfl_sync(0xffffffffu, re, wl);
-                const float bim = __shfl_sync(0xffffffffu, im, wl);
-                if (lane == 0)
-                    s_best[quad * TC_BN + col] = make_uint4(mx, static_cast<unsigned>(32 * quad + wl),
-                                                            __float_as_uint(bre), __float_as_uint(bim));
-            }
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        {
-            const int col = gt;  // 256 epilogue threads, one column each
-            const int rho = row0 + col;
-            uint4 b = s_best[col];
-            for (int qd = 1; qd < 4; ++qd) {
-                const uint4 o = s_best[qd * TC_BN + col];
-                if (o.x > b.x) b = o;  // strictly greater: lower quadrant (lower q) wins ties
-            }
-            if (rho < fa.rows && b.x != 0u) {
-                const int qb = q0 + static_cast<int>(b.y >> 1);
-                const int fb = qb / fa.D, jb = qb - fb * fa.D;
-                const int c_local = rho / fa.R_slice;
-                const int r_local = rho - c_local * fa.R_slice;
+            if (lane == 0) mbar_arrive(tempty0 + 8 * ab);
+            if (rvalid && best.lidx != 0xffffffffu) {
+                const unsigned fb = best.lidx / static_cast<unsigned>(fa.D);
+                const unsigned jb = best.lidx - fb * static_cast<unsigned>(fa.D);
                 const unsigned long long flat =
-                    (((fa.c_begin + c_local) * fa.F + fb) * fa.R_total +
-                     static_cast<unsigned long long>(fa.row_begin + r_local)) *
-                        fa.D +
-                    jb;
-                peak_publish(fa.slots + r_local, __uint_as_float(b.z), __uint_as_float(b.w), flat);
+                    ((c_glob * fa.F + fb) * fa.R_total + static_cast<unsigned long long>(r_glob)) * fa.D + jb;
+                peak_publish(fa.slots + r_local, best.re, best.im, flat);
             }
         }
     }
@@ -420,7 +423,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_BN));
+    }
+}
+
+// H_f(m) = exp(+j 4pi/lambda * kappa * sum_axes val * t^ord) for every fine
+// cell f (mixed radix over the fine axes, last fastest), phase in FP64 cycles.
+__global__ void build_htab_kernel(TcArgs a, float2* htab) {
+    const size_t total = static_cast<size_t>(a.f.F) * a.M;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(i % a.M);
+        long long rem = static_cast<long long>(i / a.M);
+        const double t = static_cast<double>(m + 1) * a.inv_prf;
+        double cyc = 0.0;
+        for (int ax = a.nfa - 1; ax >= 0; --ax) {
+            const int idx = static_cast<int>(rem % a.fcount[ax]);
+            rem /= a.fcount[ax];
+            double tp = 1.0;
+            for (int p = 0; p < a.ford[ax]; ++p) tp *= t;
+            cyc += a.coef_cycles * (a.fstart[ax] + a.fstep[ax] * idx) * tp;
+        }
+        const double fr = cyc - rint(cyc);
+        float s, c;
+        sincospif(static_cast<float>(2.0 * fr), &s, &c);
+        htab[i] = make_float2(c, s);
     }
 }
 
@@ -448,10 +475,10 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
     return false;  // AUTO: CUDA-core FFT path (see DESIGN.md for the per-shape choice)
 }
 
-inline size_t tc_smem_bytes(int terms, int tab_f, int M) {
+inline size_t tc_smem_bytes(int terms, int M) {
     const size_t stages = terms == 3 ? static_cast<size_t>(tc_stages<3>()) * tc_stage_bytes<3>()
                                      : static_cast<size_t>(tc_stages<1>()) * tc_stage_bytes<1>();
-    return 1024 + stages + (static_cast<size_t>(tab_f) + 1) * M * sizeof(float2) + 8 * (2 * 4 + 1) + 16;
+    return 1024 + stages + static_cast<size_t>(M) * sizeof(float2) + 8 * (2 * 4 + 4) + 16;
 }
 
 }  // namespace ltcib
