@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             int dq[2];
             const float2* Hq[2];
             bool vq[2];
+            float2 wd[2];  // w_M^d: per-pulse step of the Doppler phase
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int qc = q0 + qa + 64 * u;
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int jj = vq[u] ? qc - f * fa.D : 0;
                 dq[u] = jj + fa.dop_first - M / 2;
                 Hq[u] = a.htab + static_cast<size_t>(f) * M;
+                wd[u] = s_W[dq[u] & (M - 1)];
             }
             for (int kb = 0; kb < nkb; ++kb, ++it) {
                 const int s = it % STAGES;
@@ -331,10 +333,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     for (int hh = 0; hh < 2; ++hh) {
                         const int c = c_base + 4 * hh;
                         uint32_t h0[4], h1[4], l0[4], l1[4];
+                        const int mf = m0 + 4 * c;
+                        // one exact table value per 4-pulse chunk, then w_M^d steps
+                        // (3 complex products, < 3e-7 relative)
+                        float2 wv = s_W[(dq[u] * mf) & (M - 1)];
+                        const float4 hA = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf));
+                        const float4 hB = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf + 2));
+                        const float2 hv[4] = {make_float2(hA.x, hA.y), make_float2(hA.z, hA.w),
+                                              make_float2(hB.x, hB.y), make_float2(hB.z, hB.w)};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const int m = m0 + 4 * c + e;
-                            float2 b = cmul(__ldg(Hq[u] + m), s_W[(dq[u] * m) & (M - 1)]);
+                            float2 b = cmul(hv[e], wv);
+                            if (e < 3) wv = cmul(wv, wd[u]);
                             if (!vq[u]) b = make_float2(0.f, 0.f);
                             const uint32_t hb = pack_half2(b.x, b.y);     // (Br, Bi) hi
                             h0[e] = hb ^ 0x80000000u;                     // (Br, -Bi)
