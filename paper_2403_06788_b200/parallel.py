@@ -1,0 +1,140 @@
+"""Multi-GPU range-cell sharding.
+
+Every (coarse cell, ROI row) output of the cascade is independent, so ranks
+own contiguous slices of ROI rows (``shard_rows``): each replicates the echo,
+runs the coarse stage storing only its rows and the fine stage on them, and
+reduces into its own per-cell peak records.  The only exchange is gathering:
+
+* per-cell peak map: fixed-size 16-byte records {f32 re, f32 im, u64 flat
+  index} per row -> ``all_gather`` (rows are disjoint, no arithmetic);
+* candidates: counts, then a padded ``all_gather`` of records, merged and
+  re-sorted by flat index (r is not the slowest axis of the flat index);
+* global argmax: max over the gathered peaks with the reference's total order
+  (magnitude desc, flat index asc; proj/src/detectors.cpp:34-50).
+
+The collectives run through ``torch.distributed`` (NCCL between GPUs; gloo in
+the CPU tests).  ``merge_rank_maps`` is the deterministic host-side merge used
+by both; results are bit-identical for any rank count.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .model import DetectionMap
+
+
+def shard_rows(R: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous [lo, hi) slice of R ROI rows for ``rank`` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("shard_rows: bad world/rank")
+    return rank * R // world, (rank + 1) * R // world
+
+
+def _mag2_f32(v: np.ndarray) -> np.ndarray:
+    # magnitude order used everywhere on the device: fmaf(re, re, im*im) in fp32
+    re = v.real.astype(np.float32)
+    im = v.imag.astype(np.float32)
+    return (re * re + im * im).astype(np.float32)
+
+
+def argmax_total_order(index: np.ndarray, value: np.ndarray) -> int:
+    """Position of the strongest cell, ties to the lowest flat index."""
+    if index.size == 0:
+        return -1
+    m = np.abs(value)
+    best = np.max(m)
+    cand = np.nonzero(m == best)[0]
+    return int(cand[np.argmin(index[cand])])
+
+
+def merge_rank_maps(maps: Sequence[DetectionMap], full_counters: Optional[tuple] = None) -> DetectionMap:
+    """Merge per-rank maps (rank order = row order) into the single-GPU map."""
+    if not maps:
+        raise ValueError("merge_rank_maps: no maps")
+    base = maps[0]
+    out = DetectionMap(kind=base.kind, params=base.params, axes=list(base.axes),
+                       counters=full_counters if full_counters is not None else base.counters,
+                       retain_threshold=base.retain_threshold, dual=base.dual, amb=base.amb,
+                       doppler_first=base.doppler_first)
+    out.peak_index = np.concatenate([m.peak_index for m in maps])
+    out.peak_value = np.concatenate([m.peak_value for m in maps])
+    ci = np.concatenate([m.cand_index for m in maps]) if maps else np.zeros(0, np.uint64)
+    cv = np.concatenate([m.cand_value for m in maps]) if maps else np.zeros(0, np.complex128)
+    order = np.argsort(ci, kind="stable")
+    out.cand_index, out.cand_value = ci[order], cv[order]
+    k = argmax_total_order(out.peak_index, out.peak_value)
+    if k >= 0:
+        out.argmax = int(out.peak_index[k])
+        out.argmax_value = complex(out.peak_value[k])
+    return out
+
+
+def gather_map(local: DetectionMap, group=None, device=None) -> Optional[DetectionMap]:
+    """All-gather every rank's peaks and candidates; rank 0 returns the merged
+    map, other ranks return None.  Works with NCCL (device tensors) and gloo."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = device if device is not None else torch.device("cpu")
+
+    def pack(idx: np.ndarray, val: np.ndarray, n: int) -> "torch.Tensor":
+        rec = np.zeros((n, 4), np.float64)  # idx (as int64 bits), re, im, valid
+        rec[: idx.size, 0] = idx.astype(np.int64).view(np.float64)
+        rec[: idx.size, 1] = val.real
+        rec[: idx.size, 2] = val.imag
+        rec[: idx.size, 3] = 1.0
+        return torch.from_numpy(rec).to(dev)
+
+    def unpack(t: "torch.Tensor"):
+        a = t.cpu().numpy()
+        keep = a[:, 3] == 1.0
+        return a[keep, 0].copy().view(np.int64).astype(np.uint64), a[keep, 1] + 1j * a[keep, 2]
+
+    # sizes first (peaks: rows per rank; candidates: counts)
+    sizes = torch.tensor([local.peak_index.size, local.cand_index.size], dtype=torch.int64, device=dev)
+    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    all_sizes = [s.cpu().numpy() for s in all_sizes]
+    pmax = max(int(s[0]) for s in all_sizes)
+    cmax = max(int(s[1]) for s in all_sizes)
+    peaks = pack(local.peak_index, local.peak_value, pmax)
+    cands = pack(local.cand_index, local.cand_value, max(cmax, 1))
+    pg = [torch.zeros_like(peaks) for _ in range(world)]
+    cg = [torch.zeros_like(cands) for _ in range(world)]
+    dist.all_gather(pg, peaks, group=group)
+    dist.all_gather(cg, cands, group=group)
+    if rank != 0:
+        return None
+    maps = []
+    for r in range(world):
+        m = DetectionMap(kind=local.kind, params=local.params, axes=list(local.axes), counters=local.counters,
+                         retain_threshold=local.retain_threshold, dual=local.dual, amb=local.amb,
+                         doppler_first=local.doppler_first)
+        m.peak_index, m.peak_value = unpack(pg[r])
+        m.cand_index, m.cand_value = unpack(cg[r])
+        maps.append(m)
+    return merge_rank_maps(maps, local.counters)
+
+
+def split_map_by_rows(full: DetectionMap, R: int, D: int, world: int) -> List[DetectionMap]:
+    """Test helper: the per-rank maps a row-sharded run produces, cut from a full map."""
+    out = []
+    r_of = (full.cand_index // np.uint64(D)) % np.uint64(R)
+    for rank in range(world):
+        lo, hi = shard_rows(R, world, rank)
+        m = DetectionMap(kind=full.kind, params=full.params, axes=list(full.axes), counters=full.counters,
+                         retain_threshold=full.retain_threshold, dual=full.dual, amb=full.amb,
+                         doppler_first=full.doppler_first)
+        m.peak_index = full.peak_index[lo:hi].copy()
+        m.peak_value = full.peak_value[lo:hi].copy()
+        sel = (r_of >= lo) & (r_of < hi)
+        m.cand_index = full.cand_index[sel].copy()
+        m.cand_value = full.cand_value[sel].copy()
+        k = argmax_total_order(m.peak_index, m.peak_value)
+        m.argmax, m.argmax_value = int(m.peak_index[k]), complex(m.peak_value[k])
+        out.append(m)
+    return out

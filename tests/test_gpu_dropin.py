@@ -1,0 +1,28 @@
+"""The reference's own acceptance suite (proj/tests/acceptance/acceptance.cpp)
+relinked against the B200 drop-in (oracle/Makefile target `dropin`): every
+call to ltci::ds_grft / ltci::ds_kt_mfp inside it runs on the GPU, every
+other function (fd_grft_point, kt_mfp_point, keystone, extract_detections,
+synthesis) is the reference's own.  Criteria exercising the hot path:
+  2 peak law, 3 DS-GRFT factorization (100 random targets),
+  4 DS-KT-MFP factorization (100), 9 full-scale three-target scene."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_dropin")
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not os.path.exists(BIN), reason="drop-in acceptance binary not built")]
+
+
+@pytest.mark.parametrize("criterion", [2, 3, 4, 9])
+def test_reference_acceptance_through_dropin(criterion):
+    env = dict(os.environ, LTCI_THREADS=str(os.cpu_count() or 1))
+    r = subprocess.run([BIN, str(criterion)], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert f"PASS  criterion {criterion:2d}" in r.stdout
