@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--pfa", type=float, default=1e-6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample length")
+    ap.add_argument("--coarse-slice", type=int, default=0,
+                    help="restrict the coarse-velocity axis (rate measurement of configs too large for one step)")
     return ap.parse_args()
 
 
@@ -189,6 +191,8 @@ def main():
     ws, rank, local = dist_env()
     from paper_2403_06788_b200 import configs
     w = configs.config(args.config)
+    if args.coarse_slice:
+        w = configs.sliced(w, args.coarse_slice)
     if args.impl == "reference":
         run_reference(args, w, ws, rank)
         return
@@ -210,28 +214,41 @@ def main():
     gamma = detection_threshold(p, w.sigma2, args.pfa)
     opt = DetectorOptions(retain_threshold=gamma, fine_path=fine_path, device=local)
     R = s.roi.count()
-    lo, hi = rank * R // ws, (rank + 1) * R // ws
+    cpis = w.cpis
+    if cpis > 1:
+        # CPI-level data parallelism (configs[4]): each rank streams its CPIs, full ROI
+        lo, hi = 0, R
+        my_cpis = list(range(rank * cpis // ws, (rank + 1) * cpis // ws))
+    else:
+        # one CPI sharded over range start cells
+        lo, hi = rank * R // ws, (rank + 1) * R // ws
+        my_cpis = [0]
     eng = Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi)
     hyp, integ = eng.work()
 
-    cube = scene.to_complex64_roundtrip(w.cube())  # (M, K): column-major K x M
-    d_cube = torch.from_numpy(cube.astype(np.complex64)).to(dev)
+    cubes = [scene.to_complex64_roundtrip(w.cube(cpi=c)) for c in my_cpis]  # (M, K): column-major K x M
+    d_cubes = [torch.from_numpy(c.astype(np.complex64)).to(dev) for c in cubes]
+    cube = cubes[0]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     peak_ptr, n_rows = eng.peaks_device()
     peaks = torch.as_tensor(_CAI(peak_ptr, (n_rows, 4), "<u4"), device=dev)
     gathered = torch.empty((ws * (R // ws + 1), 4), dtype=torch.int32, device=dev) if ws > 1 else None
+    per_cpi_peaks = torch.empty((len(my_cpis), n_rows, 4), dtype=torch.int32, device=dev)
 
     def gather_peaks():
-        if ws > 1:
+        if ws > 1 and cpis == 1:
             # slices differ by at most one row: pad to a common length
             pad = torch.zeros((R // ws + 1, 4), dtype=torch.int32, device=dev)
             pad[:n_rows].copy_(peaks.view(torch.int32))
             dist.all_gather_into_tensor(gathered, pad)
 
     def step():
-        eng.run_device(d_cube.data_ptr(), sptr)
+        for i, dc in enumerate(d_cubes):
+            eng.run_device(dc.data_ptr(), sptr)
+            if cpis > 1:
+                per_cpi_peaks[i].copy_(peaks.view(torch.int32))  # keep each CPI's peak map
         gather_peaks()
 
     for _ in range(max(3, args.warmup)):
@@ -259,33 +276,36 @@ def main():
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    total_integ = w.integrations()  # all ranks together cover every hypothesis once
+    total_integ = w.integrations() * cpis  # all ranks together cover every hypothesis of every CPI once
     value = total_integ * args.steps / (ms_max * 1e-3) / 1e9
+    cpi_rate = cpis * args.steps / (ms_max * 1e-3)
 
     # ---- kernel split (timed pass) for the roofline
     eng.set_timing(True)
     flush.zero_()
-    eng.run_device(d_cube.data_ptr(), sptr)
+    eng.run_device(d_cubes[0].data_ptr(), sptr)
     st = eng.stats()
     eng.set_timing(False)
-    launches = st["launches"]
+    launches = st["launches"] * len(my_cpis)
 
     # ---- e2e: public API from pinned host memory, results back to host
-    host = torch.from_numpy(cube.view(np.float64).reshape(-1)).pin_memory()
+    hosts = [torch.from_numpy(c.view(np.float64).reshape(-1)).pin_memory() for c in cubes]
     e2e_ms = []
     d2h = 0
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        eng.run_host_ptr(host.data_ptr(), sptr)
-        m = eng.result(sptr)
+        d2h = 0
+        for hst in hosts:
+            eng.run_host_ptr(hst.data_ptr(), sptr)
+            m = eng.result(sptr)
+            d2h += 8 + 16 * n_rows + 16 * int(m.cand_index.size)
         if ws > 1:
             gather_peaks()
             torch.cuda.synchronize(dev)
         t1 = time.perf_counter()
         if i >= args.warmup:
             e2e_ms.append((t1 - t0) * 1e3)
-        d2h = 8 + 16 * n_rows + 16 * int(m.cand_index.size)
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -306,35 +326,58 @@ def main():
         else:
             coarse = w.amb.count() * s.coarse[1].count
             fine_cells = s.fine[1].count
-        per_launch_flops = coarse * (hi - lo) * fine_cells * fft_flops_per_row_cell(p.M, D)
-        achieved = per_launch_flops / (st["fine_ms"] * 1e-3) / 1e12
+        rows_here = (hi - lo)
         hbm = peaks_json.get("hbm_gbs", 6650.0)
-        x_bytes = 8.0 * coarse * (hi - lo) * p.M + 8.0 * p.K * p.M
+        x_bytes = 8.0 * coarse * rows_here * p.M + 8.0 * p.K * p.M
         coarse_gbs = x_bytes / (st["coarse_ms"] * 1e-3) / 1e9 if st["coarse_ms"] > 0 else None
+        use_tc = args.fine_path in ("tc", "tcfast") or (args.fine_path == "auto" and p.M > 1024)
+        terms = 1 if args.fine_path == "tcfast" else 3
+        fine_s = st["fine_ms"] * 1e-3
+        if use_tc:
+            peak_tc = peaks_json.get("bf16_tflops_sustained", 1394.2)
+            achieved = 8.0 * integ / fine_s / 1e12  # algorithmic: 8 flop per integration
+            roof = {"bound": "tensor", "kernel": f"fine_tc_kernel<{terms}> (K2a+K3, tcgen05)",
+                    "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s", "frac": achieved / peak_tc,
+                    "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside seconds-long steps)",
+                    "algorithmic": "8 flop per hypothesis x pulse integration (complex MAC)",
+                    "executed_tflops": terms * achieved, "executed_frac": terms * achieved / peak_tc,
+                    "split_terms": terms}
+        else:
+            per_launch_flops = coarse * rows_here * fine_cells * fft_flops_per_row_cell(p.M, D)
+            achieved = per_launch_flops / fine_s / 1e12
+            roof = {"bound": "fp32", "kernel": "fine_fft_kernel (K2b+K3, CUDA cores)",
+                    "achieved": achieved, "peak": fp32.value, "unit": "TFLOP/s",
+                    "frac": achieved / fp32.value if fp32.value else None, "traffic": None,
+                    "peak_source": "measured in-run FFMA chain microbenchmark (ltci_cuda_measure_fp32_peak)",
+                    "algorithmic": "per (row, fine cell): 6M chirp + 5M log2M FFT + 3D |Y|^2 flop",
+                    "dense_equiv_tflops": 8.0 * integ / fine_s / 1e12}
+        roof.update({"fine_ms": st["fine_ms"], "coarse_ms": st["coarse_ms"], "keystone_ms": st["keystone_ms"],
+                     "fine_share": st["fine_ms"] / max(1e-9, st["fine_ms"] + st["coarse_ms"] + st["keystone_ms"]),
+                     "coarse_stage": {"bound": "hbm", "achieved": coarse_gbs, "peak": hbm, "unit": "GB/s",
+                                      "frac": coarse_gbs / hbm if coarse_gbs else None,
+                                      "algorithmic": "8 B x (K M echo + coarse x R x M X write)"}})
+        name = "DS-GRFT" if w.variant == 0 else "DS-KT-MFP"
+        if cpis > 1:
+            metric, unit, val, e2e_val = f"{name} CPIs/s ({cpis}-CPI stream)", "CPI/s", cpi_rate, \
+                cpis * args.steps / (float(e2e_t.item()) * 1e-3)
+        else:
+            metric, unit, val, e2e_val = f"{name} motion-hypothesis x pulse integrations/s", "G/s", value, e2e_value
         line = {
-            "metric": "DS-GRFT motion-hypothesis x pulse integrations/s" if w.variant == 0 else
-                      "DS-KT-MFP motion-hypothesis x pulse integrations/s",
-            "value": value, "unit": "G/s", "n_gpus": ws, "steps": args.steps, "warmup": max(3, args.warmup),
-            "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "c64 (fp32)",
+            "metric": metric, "value": val, "unit": unit, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
+            "dtype": "c64 / fp32" if not use_tc else ("fp16x3 split (FP32 class)" if terms == 3 else "fp16"),
             "data": "synthetic (seeded reference signal model: CN(0,1) range noise + targets)",
-            "config": {"workload": w.name, "config_index": args.config, "K": p.K, "M": p.M,
-                       "hypotheses": w.hypotheses(), "integrations_per_step": total_integ,
-                       "parallelism": f"range-cell shards x{ws}" if ws > 1 else "single GPU",
+            "config": {"workload": w.name, "config_index": args.config, "K": p.K, "M": p.M, "cpis": cpis,
+                       "hypotheses_per_cpi": w.hypotheses(), "integrations_per_step": total_integ,
+                       "integrations_per_s_G": value,
+                       "parallelism": ("CPI shards" if cpis > 1 else "range-cell shards") + f" x{ws}",
                        "retain_threshold": gamma, "pfa": args.pfa,
-                       "l2": "flushed between steps (512 MiB write, untimed); X stream 5.6 GB >> L2",
-                       "fine_path": args.fine_path},
-            "roofline": {"bound": "fp32", "kernel": "fine_fft_kernel (K2b+K3)",
-                         "achieved": achieved, "peak": fp32.value, "unit": "TFLOP/s",
-                         "frac": achieved / fp32.value if fp32.value else None, "traffic": None,
-                         "peak_source": "measured in-run FFMA chain microbenchmark (ltci_cuda_measure_fp32_peak)",
-                         "algorithmic": "per (row, fine cell): 6M chirp + 5M log2M FFT + 3D |Y|^2 flop",
-                         "fine_ms": st["fine_ms"], "coarse_ms": st["coarse_ms"],
-                         "coarse_stage": {"bound": "hbm", "achieved": coarse_gbs, "peak": hbm, "unit": "GB/s",
-                                          "frac": coarse_gbs / hbm if coarse_gbs else None,
-                                          "algorithmic": "8 B x (K M echo + coarse x R x M X write)"},
-                         "dense_equiv_tflops": 8.0 * integ / (st["fine_ms"] * 1e-3) / 1e12},
-            "e2e": {"value": e2e_value, "unit": "G/s", "h2d_bytes_per_step": int(cube.size * 16),
+                       "l2": "flushed between steps (512 MiB write, untimed); X stream >> L2",
+                       "fine_path": args.fine_path + (" -> tcgen05" if use_tc else " -> cuda-core fft")},
+            "roofline": roof,
+            "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": int(cube.size * 16 * len(cubes)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms))},
             "gpu_launches": int(launches) * args.steps,
             "clocks": clk.summary(),

@@ -178,9 +178,13 @@ void check_grids(const ltci_dual_space& s) {
             fail(LTCI_INVALID_ARGUMENT, "dual-scale space: empty grid");
 }
 
-void check_supported(const ltci_radar& r) {
-    if (r.M < 4 || r.M > 1024)
-        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: pulse count M must be a power of two in [4, 1024]");
+void check_supported(const ltci_radar& r, int fine_path = LTCI_FINE_AUTO) {
+    // CUDA-core FFT path: M in [4, 1024]; tcgen05 path: M in [32, 2048]
+    const bool tc = fine_path == LTCI_FINE_TC_DENSE || fine_path == LTCI_FINE_TC_FAST ||
+                    (fine_path == LTCI_FINE_AUTO && r.M > 1024);
+    if (r.M < 4 || r.M > 2048 || (!tc && r.M > 1024) || (tc && r.M < 32))
+        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: pulse count M must be a power of two in [4, 1024] "
+                                    "(CUDA-core path) or [32, 2048] (tcgen05 path)");
     if (r.K < 16 || r.K > 8192)
         fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be a power of two in [16, 8192]");
 }
@@ -198,7 +202,7 @@ Plan make_plan(const ltci_radar& cube_params, const ltci_dual_space& s, const lt
     if (variant == LTCI_VARIANT_KTMFP && !amb) fail(LTCI_INVALID_ARGUMENT, "ds_kt_mfp: ambiguity space required");
     check_grids(s);
     check_roi(s);
-    check_supported(cube_params);
+    check_supported(cube_params, opt ? opt->fine_path : LTCI_FINE_AUTO);
     const int M = pl.rp.M;
     pl.kappa = s.kappa;
     pl.R_total = s.roi_last - s.roi_first + 1;

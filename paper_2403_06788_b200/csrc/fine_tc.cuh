@@ -13,23 +13,27 @@
 // depend on the coarse cell, so the whole stage is one GEMM.
 //
 // Real-ified with complex interleaving along K (k' = 2m + {re, im}):
-//   A operand (MMA M = 128): generated steering tile, row n' = 2q + part,
+//   A operand (MMA M = 128): X rows, K-major fp16, loaded by TMA (SW128);
+//   B operand (MMA N = 256): generated steering tile, row n' = 2q + part,
 //        part 0 -> (Br, -Bi), part 1 -> (Bi, Br) at (k' = 2m, 2m + 1);
-//   B operand (MMA N = 256): X rows, K-major fp16, loaded by TMA (SW128);
-//   D (TMEM, fp32, 128 lanes x 256 columns): Re Y at even lanes, Im Y at odd.
+//   D (TMEM, fp32, 128 lanes x 256 columns): lane = X row, Re Y / Im Y of
+//        output q in adjacent columns 2q, 2q + 1.
 // Split precision: x = x_hi + x_lo in fp16 (global power-of-two prescale s
-// keeps X in fp16's normal range); TERMS = 3 accumulates A_hi X_hi + A_lo X_hi
-// + A_hi X_lo (error ~1e-7 rel., FP32 class); TERMS = 1 is A_hi X_hi (~3e-4 of
+// keeps X in fp16's normal range); TERMS = 3 accumulates X_hi G_hi + X_hi G_lo
+// + X_lo G_hi (error ~1e-7 rel., FP32 class); TERMS = 1 is X_hi G_hi (~3e-4 of
 // the row maximum, inside the 1e-3 contract; opt-in).
 //
-// Warp roles (320 threads, one CTA per (64 complex outputs) x (256 rows) tile):
-//   warp 0     TMEM allocation; one lane issues the TMA loads of X tiles
-//   warp 1     one lane issues tcgen05.mma and tcgen05.commit
-//   warps 2-9  generate the steering tile in swizzled smem from per-CTA
-//              tables (H_f(m) evaluated in FP64 cycles, w_M^k exact-index
-//              table), then run the epilogue: tcgen05.ld, |Y|^2, threshold
-//              compaction, per-row argmax (redux.sync + ballot, ties to the
-//              lowest q), one 128-bit CAS per row into the per-cell peak slot.
+// Persistent CTAs (one per SM) walk (128-row, 128-output) tiles; warp roles
+// (448 threads):
+//   warp 0      TMEM allocation (512 columns = two accumulators); one lane
+//               issues the TMA loads of X tiles
+//   warp 1      one lane issues tcgen05.mma / tcgen05.commit
+//   warps 2-9   generate the steering tile in swizzled smem from the FP64
+//               H table (global, L1-resident per tile) and w_M^k
+//   warps 10-13 epilogue, one X row per thread: tcgen05.ld, |Y|^2, threshold
+//               compaction, in-thread row argmax (lowest q on ties), one
+//               128-bit CAS per row and tile into the per-cell peak slot;
+//               overlaps the next tile's MMAs (double-buffered TMEM).
 #pragma once
 
 #include <cuda.h>
@@ -482,7 +486,9 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
         if (M < 32) throw std::invalid_argument("ltci_cuda: tcgen05 fine path needs M >= 32");
         return true;
     }
-    return false;  // AUTO: CUDA-core FFT path (see DESIGN.md for the per-shape choice)
+    // AUTO: the CUDA-core FFT path up to M = 1024 (measured faster than the
+    // 3-term tensor path at C1); beyond it the tensor path.
+    return M > 1024;
 }
 
 inline size_t tc_smem_bytes(int terms, int M) {
