@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample length")
     ap.add_argument("--coarse-slice", type=int, default=0,
                     help="restrict the coarse-velocity axis (rate measurement of configs too large for one step)")
+    ap.add_argument("--coarse-rest", type=int, default=0, help="with --coarse-slice: restrict the other coarse axes")
     return ap.parse_args()
 
 
@@ -192,7 +193,7 @@ def main():
     from paper_2403_06788_b200 import configs
     w = configs.config(args.config)
     if args.coarse_slice:
-        w = configs.sliced(w, args.coarse_slice)
+        w = configs.sliced(w, args.coarse_slice, args.coarse_rest)
     if args.impl == "reference":
         run_reference(args, w, ws, rank)
         return

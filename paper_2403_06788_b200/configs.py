@@ -155,13 +155,18 @@ def config(i: int) -> Workload:
     raise ValueError(f"no BASELINE config {i}")
 
 
-def sliced(w: Workload, coarse_v: int) -> Workload:
-    """Same workload restricted to the first ``coarse_v`` coarse-velocity cells
-    (bounded CPU-baseline samples; every coarse cell costs the same)."""
+def sliced(w: Workload, coarse_v: int, coarse_rest: int = 0) -> Workload:
+    """Same workload restricted to the first ``coarse_v`` cells of the leading
+    coarse axis (and, if ``coarse_rest``, of every other coarse axis) -- bounded
+    samples for rate measurements; every coarse cell costs the same."""
     import copy
     w2 = copy.deepcopy(w)
     axis = 0 if w.variant == 0 else 1
     g = w2.space.coarse[axis]
     g.count = min(g.count, coarse_v)
-    w2.name = f"{w.name} [coarse slice {coarse_v}]"
+    if coarse_rest:
+        for i, gg in enumerate(w2.space.coarse):
+            if i != axis:
+                gg.count = min(gg.count, coarse_rest)
+    w2.name = f"{w.name} [coarse slice {coarse_v}" + (f"x{coarse_rest}" if coarse_rest else "") + "]"
     return w2
