@@ -170,6 +170,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// exp(+j 2 pi idx / M) for an exact integer index (reduced to [-M/2, M/2), so
+// the MUFU argument stays in [-pi, pi): abs error < 4e-7).
+__device__ __forceinline__ float2 wpow(int idx, int M) {
+    int k = idx & (M - 1);
+    if (k >= M / 2) k -= M;
+    float s, c;
+    __sincosf(6.28318530717958647692f * static_cast<float>(k) / static_cast<float>(M), &s, &c);
+    return make_float2(c, s);
+}
+
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -208,8 +218,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const FineArgs& fa = a.f;
     const int M = a.M;
-    float2* s_W = reinterpret_cast<float2*>(smem + STAGES * SB);         // [M]  w_M^k
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_W + M);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -236,11 +245,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                      "r"(2 * TC_BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    for (int k = threadIdx.x; k < M; k += TC_THREADS) {
-        float s, c;
-        sincospif(2.0f * static_cast<float>(k) / static_cast<float>(M), &s, &c);
-        s_W[k] = make_float2(c, s);
     }
     tc_fence_before();
     __syncthreads();
@@ -298,28 +302,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
     } else if (warp < 2 + TC_GEN_WARPS) {
         // ---------------- steering generators (MMA B operand) ----------------
-        // thread -> (q_local, 16-byte chunk) items; every complex steering value
-        // is computed once and written to both of its real rows
-        // (2q: (Br, -Bi) -> Re Y, 2q+1: (Bi, Br) -> Im Y).
-        const int gt = threadIdx.x - 64;              // 0..255
-        const int qa = (gt & 7) + 8 * (gt >> 5);      // 0..63, second item at qa + 64
-        const int c_base = (gt >> 3) & 3;             // chunks c_base, c_base + 4
+        // Each complex steering value is computed once and written to both of
+        // its real rows (2q: (Br, -Bi) -> Re Y, 2q+1: (Bi, Br) -> Im Y).
+        // Lane bits 0-1 pick the q (row swizzle residue), bits 2-4 the 16-byte
+        // chunk, so every 8-lane phase of a 128-bit store hits 8 distinct bank
+        // groups; 4 passes of 32 q per warp cover the 128 q of a tile.
+        const int wg = warp - 2;                       // 0..7
+        const int c = lane >> 2;                       // chunk 0..7 (4 pulses each)
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int q0 = (t % nq) * TC_QT;
-            int dq[2];
-            const float2* Hq[2];
-            bool vq[2];
-            float2 wd[2];  // w_M^d: per-pulse step of the Doppler phase
+            int dq[4];
+            const float2* Hq[4];
+            bool vq[4];
+            float2 wd[4];  // w_M^d: per-pulse step of the Doppler phase
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int qc = q0 + qa + 64 * u;
+            for (int u = 0; u < 4; ++u) {
+                const int qc = q0 + (lane & 3) + 4 * wg + 32 * u;
                 vq[u] = qc < Q;
                 const int f = vq[u] ? qc / fa.D : 0;
                 const int jj = vq[u] ? qc - f * fa.D : 0;
                 dq[u] = jj + fa.dop_first - M / 2;
                 Hq[u] = a.htab + static_cast<size_t>(f) * M;
-                wd[u] = s_W[dq[u] & (M - 1)];
+                wd[u] = wpow(dq[u], M);
             }
             for (int kb = 0; kb < nkb; ++kb, ++it) {
                 const int s = it % STAGES;
@@ -327,47 +332,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 mbar_wait(empty0 + 8 * s, ph ^ 1);
                 uint8_t* g_hi = smem + s * SB + PLANES * TC_X_BYTES;
                 uint8_t* g_lo = g_hi + TC_G_BYTES;
-                const int m0 = kb * (TC_BK / 2);
+                const int mf = kb * (TC_BK / 2) + 4 * c;
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int L0 = 2 * (qa + 64 * u), L1 = L0 + 1;
-                    const uint32_t r0 = (L0 >> 3) * 1024 + (L0 & 7) * 128;
-                    const uint32_t r1 = (L1 >> 3) * 1024 + (L1 & 7) * 128;
+                for (int u = 0; u < 4; ++u) {
+                    const int L0 = 2 * ((lane & 3) + 4 * wg + 32 * u), L1 = L0 + 1;
+                    const uint32_t o0 = (L0 >> 3) * 1024 + (L0 & 7) * 128 + ((c ^ (L0 & 7)) << 4);
+                    const uint32_t o1 = (L1 >> 3) * 1024 + (L1 & 7) * 128 + ((c ^ (L1 & 7)) << 4);
+                    uint32_t h0[4], h1[4], l0[4], l1[4];
+                    // exact-index w_M^{d m} for the chunk's first pulse, then w_M^d steps
+                    float2 wv = wpow(dq[u] * mf, M);
+                    const float4 hA = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf));
+                    const float4 hB = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf + 2));
+                    const float2 hv[4] = {make_float2(hA.x, hA.y), make_float2(hA.z, hA.w),
+                                          make_float2(hB.x, hB.y), make_float2(hB.z, hB.w)};
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int c = c_base + 4 * hh;
-                        uint32_t h0[4], h1[4], l0[4], l1[4];
-                        const int mf = m0 + 4 * c;
-                        // one exact table value per 4-pulse chunk, then w_M^d steps
-                        // (3 complex products, < 3e-7 relative)
-                        float2 wv = s_W[(dq[u] * mf) & (M - 1)];
-                        const float4 hA = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf));
-                        const float4 hB = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf + 2));
-                        const float2 hv[4] = {make_float2(hA.x, hA.y), make_float2(hA.z, hA.w),
-                                              make_float2(hB.x, hB.y), make_float2(hB.z, hB.w)};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            float2 b = cmul(hv[e], wv);
-                            if (e < 3) wv = cmul(wv, wd[u]);
-                            if (!vq[u]) b = make_float2(0.f, 0.f);
-                            const uint32_t hb = pack_half2(b.x, b.y);     // (Br, Bi) hi
-                            h0[e] = hb ^ 0x80000000u;                     // (Br, -Bi)
-                            h1[e] = __byte_perm(hb, 0, 0x1032);           // (Bi, Br)
-                            if (TERMS == 3) {
-                                const float2 hf = unpack_half2(hb);
-                                const uint32_t lb = pack_half2(b.x - hf.x, b.y - hf.y);
-                                l0[e] = lb ^ 0x80000000u;
-                                l1[e] = __byte_perm(lb, 0, 0x1032);
-                            }
-                        }
-                        const uint32_t o0 = r0 + ((c ^ (L0 & 7)) << 4);
-                        const uint32_t o1 = r1 + ((c ^ (L1 & 7)) << 4);
-                        *reinterpret_cast<uint4*>(g_hi + o0) = make_uint4(h0[0], h0[1], h0[2], h0[3]);
-                        *reinterpret_cast<uint4*>(g_hi + o1) = make_uint4(h1[0], h1[1], h1[2], h1[3]);
+                    for (int e = 0; e < 4; ++e) {
+                        float2 b = cmul(hv[e], wv);
+                        if (e < 3) wv = cmul(wv, wd[u]);
+                        if (!vq[u]) b = make_float2(0.f, 0.f);
+                        const uint32_t hb = pack_half2(b.x, b.y);     // (Br, Bi) hi
+                        h0[e] = hb ^ 0x80000000u;                     // (Br, -Bi)
+                        h1[e] = __byte_perm(hb, 0, 0x1032);           // (Bi, Br)
                         if (TERMS == 3) {
-                            *reinterpret_cast<uint4*>(g_lo + o0) = make_uint4(l0[0], l0[1], l0[2], l0[3]);
-                            *reinterpret_cast<uint4*>(g_lo + o1) = make_uint4(l1[0], l1[1], l1[2], l1[3]);
+                            const float2 hf = unpack_half2(hb);
+                            const uint32_t lb = pack_half2(b.x - hf.x, b.y - hf.y);
+                            l0[e] = lb ^ 0x80000000u;
+                            l1[e] = __byte_perm(lb, 0, 0x1032);
                         }
+                    }
+                    *reinterpret_cast<uint4*>(g_hi + o0) = make_uint4(h0[0], h0[1], h0[2], h0[3]);
+                    *reinterpret_cast<uint4*>(g_hi + o1) = make_uint4(h1[0], h1[1], h1[2], h1[3]);
+                    if (TERMS == 3) {
+                        *reinterpret_cast<uint4*>(g_lo + o0) = make_uint4(l0[0], l0[1], l0[2], l0[3]);
+                        *reinterpret_cast<uint4*>(g_lo + o1) = make_uint4(l1[0], l1[1], l1[2], l1[3]);
                     }
                 }
                 fence_proxy_async();
@@ -494,7 +491,8 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
 inline size_t tc_smem_bytes(int terms, int M) {
     const size_t stages = terms == 3 ? static_cast<size_t>(tc_stages<3>()) * tc_stage_bytes<3>()
                                      : static_cast<size_t>(tc_stages<1>()) * tc_stage_bytes<1>();
-    return 1024 + stages + static_cast<size_t>(M) * sizeof(float2) + 8 * (2 * 4 + 4) + 16;
+    (void)M;
+    return 1024 + stages + 8 * (2 * 4 + 4) + 16;
 }
 
 }  // namespace ltcib
