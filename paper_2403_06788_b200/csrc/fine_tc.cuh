@@ -84,6 +84,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 }
 
 // Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+// try_wait carries a suspend-time hint, so a waiting warp sleeps in hardware
+// until the phase completes instead of spinning on issue slots the generator
+// warps need.
 __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
     const long long t0 = clock64();
 #pragma unroll 1
@@ -91,10 +94,10 @@ __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
         uint32_t done;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(bar), "r"(parity)
+            : "r"(bar), "r"(parity), "r"(1000000u)
             : "memory");
         if (done) return;
         if (clock64() - t0 > 20000000000ll) __trap();  // ~10 s: protocol bug, fail the launch
