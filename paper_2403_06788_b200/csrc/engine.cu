@@ -377,7 +377,31 @@ CUtensorMap make_x16_map(void* base, int M, unsigned long long rows) {
 }
 
 template <int TERMS>
+void launch_tc2_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& lo, cudaStream_t st) {
+    auto kern = fine_tc2_kernel<TERMS>;
+    const size_t smem = tc2_smem_bytes(TERMS);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const long long Q = static_cast<long long>(a.f.F) * a.f.D;
+    const long long tiles = ((Q + TC_QT - 1) / TC_QT) * ((a.f.rows + 2 * TC2_BM - 1) / (2 * TC2_BM));
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int pairs = static_cast<int>(std::min<long long>(tiles, sms / 2));  // persistent CTA pairs
+    kern<<<2 * pairs, TC_THREADS, smem, st>>>(a, hi, lo);
+    CK(cudaGetLastError());
+}
+
+bool tc_pair_enabled() {
+    const char* e = std::getenv("LTCI_TC_PAIR");
+    return !(e && e[0] == '0');
+}
+
+template <int TERMS>
 void launch_tc_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& lo, cudaStream_t st) {
+    if (tc_pair_enabled()) {
+        launch_tc2_terms<TERMS>(a, hi, lo, st);
+        return;
+    }
     auto kern = fine_tc_kernel<TERMS>;
     const size_t smem = tc_smem_bytes(TERMS, a.M);
     if (smem > 227 * 1024) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: tcgen05 tiles exceed shared memory");

@@ -441,6 +441,340 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
+// ===================== CTA-pair variant (cta_group::2) =====================
+// A cluster of two CTAs on one TPC computes a 256-row x 256-column tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA loads its own 128 X rows and
+// generates HALF of the steering columns (64 complex outputs), so the
+// generator work and the smem operand reads per SM halve; D lands in each
+// CTA's TMEM as its 128 rows x 256 columns.  Protocol (CUTLASS 2-SM style):
+//   full[s]   leader's barrier: leader producer expect_tx (both CTAs' bytes),
+//             both CTAs' TMA complete_tx, 8 generator warps per CTA arrive
+//   empty[s]  per CTA: leader's tcgen05.commit multicast to both CTAs
+//   tfull[b]  per CTA: commit multicast after a tile's last k-block
+//   tempty[b] leader's barrier: 4 epilogue warps per CTA arrive
+constexpr int TC2_BM = 128;                    // X rows per CTA
+constexpr int TC2_GN = 128;                    // generated real columns per CTA (64 q)
+constexpr int TC2_X_BYTES = TC2_BM * TC_BK * 2;
+constexpr int TC2_G_BYTES = TC2_GN * TC_BK * 2;
+
+template <int TERMS>
+__host__ __device__ constexpr int tc2_stages() {
+    return TERMS == 3 ? 3 : 6;
+}
+
+template <int TERMS>
+__host__ __device__ constexpr int tc2_stage_bytes() {
+    return (TERMS == 3 ? 2 : 1) * (TC2_X_BYTES + TC2_G_BYTES);
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __noinline__ void mbar_wait_cluster_slow(uint32_t bar, uint32_t parity) {
+    const long long t0 = clock64();
+#pragma unroll 1
+    for (;;) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity), "r"(1000000u)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > 20000000000ll) __trap();
+    }
+}
+
+// wait with cluster-scope acquire (arrivals come from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (!done) mbar_wait_cluster_slow(bar, parity);
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc2_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc2_commit_both(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            bar),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
+template <int TERMS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    fine_tc2_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ CUtensorMap tm_hi,
+                    const __grid_constant__ CUtensorMap tm_lo) {
+    constexpr int STAGES = tc2_stages<TERMS>();
+    constexpr int PLANES = TERMS == 3 ? 2 : 1;
+    constexpr int SB = tc2_stage_bytes<TERMS>();
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const FineArgs& fa = a.f;
+    const int M = a.M;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int Q = static_cast<int>(fa.F) * fa.D;
+    const int nq = (Q + TC_QT - 1) / TC_QT;
+    const int nrt = (fa.rows + 2 * TC2_BM - 1) / (2 * TC2_BM);
+    const int ntiles = nq * nrt;
+    const int nkb = (2 * M) / TC_BK;
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+    const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+    const uint32_t full0_l = mapa_shared(full0, 0), tempty0_l = mapa_shared(tempty0, 0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1 + 2 * TC_GEN_WARPS);  // leader producer + generators of both CTAs
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);
+            mbar_init(tempty0 + 8 * b, 2 * TC_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                     "r"(2 * TC_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *s_tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int t = pair; t < ntiles; t += npairs) {
+                const int row0 = (t / nq) * (2 * TC2_BM) + rank * TC2_BM;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(empty0 + 8 * s, ph ^ 1);
+                    uint8_t* st = smem + s * SB;
+                    if (rank == 0) mbar_expect_tx(full0 + 8 * s, 2 * PLANES * TC2_X_BYTES);
+                    tma_load_2d_pair(smem_u32(st), &tm_hi, kb * TC_BK, row0, full0_l + 8 * s);
+                    if (TERMS == 3)
+                        tma_load_2d_pair(smem_u32(st + TC2_X_BYTES), &tm_lo, kb * TC_BK, row0, full0_l + 8 * s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = tc_idesc(2 * TC2_BM, TC_BN);
+            int it = 0, i = 0;
+            for (int t = pair; t < ntiles; t += npairs, ++i) {
+                const int ab = i & 1;
+                mbar_wait_cluster(tempty0 + 8 * ab, ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dcol = tmem + ab * TC_BN;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait_cluster(full0 + 8 * s, ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * SB);
+                    const uint32_t x_hi = st, x_lo = st + TC2_X_BYTES;
+                    const uint32_t g_hi = st + PLANES * TC2_X_BYTES, g_lo = g_hi + TC2_G_BYTES;
+#pragma unroll
+                    for (int ks = 0; ks < TC_BK / 16; ++ks) {
+                        const uint32_t off = ks * 32;
+                        tc2_mma(dcol, sw128_desc(x_hi + off), sw128_desc(g_hi + off), idesc, (kb | ks) != 0);
+                        if (TERMS == 3) {
+                            tc2_mma(dcol, sw128_desc(x_hi + off), sw128_desc(g_lo + off), idesc, 1);
+                            tc2_mma(dcol, sw128_desc(x_lo + off), sw128_desc(g_hi + off), idesc, 1);
+                        }
+                    }
+                    tc2_commit_both(empty0 + 8 * s);
+                }
+                tc2_commit_both(tfull0 + 8 * ab);
+            }
+        }
+    } else if (warp < 2 + TC_GEN_WARPS) {
+        // generators: this CTA's 64 q of the tile (q0 + 64 rank ...), 2 per thread
+        const int wg = warp - 2;
+        const int c = lane >> 2;
+        int it = 0;
+        for (int t = pair; t < ntiles; t += npairs) {
+            const int q0 = (t % nq) * TC_QT + 64 * static_cast<int>(rank);
+            int dq[2];
+            const float2* Hq[2];
+            bool vq[2];
+            float2 wd[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int qc = q0 + (lane & 3) + 4 * wg + 32 * u;
+                vq[u] = qc < Q;
+                const int f = vq[u] ? qc / fa.D : 0;
+                const int jj = vq[u] ? qc - f * fa.D : 0;
+                dq[u] = jj + fa.dop_first - M / 2;
+                Hq[u] = a.htab + static_cast<size_t>(f) * M;
+                wd[u] = wpow(dq[u], M);
+            }
+            for (int kb = 0; kb < nkb; ++kb, ++it) {
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                mbar_wait(empty0 + 8 * s, ph ^ 1);
+                uint8_t* g_hi = smem + s * SB + PLANES * TC2_X_BYTES;
+                uint8_t* g_lo = g_hi + TC2_G_BYTES;
+                const int mf = kb * (TC_BK / 2) + 4 * c;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int L0 = 2 * ((lane & 3) + 4 * wg + 32 * u), L1 = L0 + 1;
+                    const uint32_t o0 = (L0 >> 3) * 1024 + (L0 & 7) * 128 + ((c ^ (L0 & 7)) << 4);
+                    const uint32_t o1 = (L1 >> 3) * 1024 + (L1 & 7) * 128 + ((c ^ (L1 & 7)) << 4);
+                    uint32_t h0[4], h1[4], l0[4], l1[4];
+                    float2 wv = wpow(dq[u] * mf, M);
+                    const float4 hA = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf));
+                    const float4 hB = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf + 2));
+                    const float2 hv[4] = {make_float2(hA.x, hA.y), make_float2(hA.z, hA.w),
+                                          make_float2(hB.x, hB.y), make_float2(hB.z, hB.w)};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        float2 b = cmul(hv[e], wv);
+                        if (e < 3) wv = cmul(wv, wd[u]);
+                        if (!vq[u]) b = make_float2(0.f, 0.f);
+                        const uint32_t hb = pack_half2(b.x, b.y);
+                        h0[e] = hb ^ 0x80000000u;
+                        h1[e] = __byte_perm(hb, 0, 0x1032);
+                        if (TERMS == 3) {
+                            const float2 hf = unpack_half2(hb);
+                            const uint32_t lb = pack_half2(b.x - hf.x, b.y - hf.y);
+                            l0[e] = lb ^ 0x80000000u;
+                            l1[e] = __byte_perm(lb, 0, 0x1032);
+                        }
+                    }
+                    *reinterpret_cast<uint4*>(g_hi + o0) = make_uint4(h0[0], h0[1], h0[2], h0[3]);
+                    *reinterpret_cast<uint4*>(g_hi + o1) = make_uint4(h1[0], h1[1], h1[2], h1[3]);
+                    if (TERMS == 3) {
+                        *reinterpret_cast<uint4*>(g_lo + o0) = make_uint4(l0[0], l0[1], l0[2], l0[3]);
+                        *reinterpret_cast<uint4*>(g_lo + o1) = make_uint4(l1[0], l1[1], l1[2], l1[3]);
+                    }
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(full0_l + 8 * s);
+            }
+        }
+    } else {
+        // epilogue: this CTA's 128 rows, all 256 columns (128 q) of the tile
+        const int quad = warp & 3;
+        const float inv_s = 1.0f / fp16_prescale(a.maxbits, a.K);
+        int i = 0;
+        for (int t = pair; t < ntiles; t += npairs, ++i) {
+            const int ab = i & 1;
+            const int q0 = (t % nq) * TC_QT;
+            const int rho = (t / nq) * (2 * TC2_BM) + rank * TC2_BM + 32 * quad + lane;
+            const bool rvalid = rho < fa.rows;
+            const int c_local = rvalid ? rho / fa.R_slice : 0;
+            const int r_local = rho - c_local * fa.R_slice;
+            const unsigned long long c_glob = fa.c_begin + c_local;
+            const int r_glob = fa.row_begin + r_local;
+            mbar_wait(tfull0 + 8 * ab, (i >> 1) & 1);
+            tc_fence_after();
+            RowBest best{-1.0f, 0xffffffffu, 0.f, 0.f};
+            int qf = q0 / fa.D, qj = q0 - qf * fa.D;
+            for (int cb = 0; cb < TC_BN / 32; ++cb) {
+                uint32_t r[32];
+                tmem_ld32(tmem + (static_cast<uint32_t>(32 * quad) << 16) + ab * TC_BN + cb * 32, r);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int q = q0 + cb * 16 + j;
+                    const float re = __uint_as_float(r[2 * j]) * inv_s;
+                    const float im = __uint_as_float(r[2 * j + 1]) * inv_s;
+                    if (rvalid && q < Q) {
+                        const float m2 = mag2f(re, im);
+                        if (m2 > best.m) {
+                            best.m = m2;
+                            best.lidx = static_cast<unsigned>(q);
+                            best.re = re;
+                            best.im = im;
+                        }
+                        if (fa.dense != nullptr || m2 > fa.retain2)
+                            emit_cell(fa, make_float2(re, im), m2, static_cast<unsigned>(qf), qj, c_glob, r_glob,
+                                      fa.dense != nullptr);
+                    }
+                    if (++qj == fa.D) {
+                        qj = 0;
+                        ++qf;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty0_l + 8 * ab);
+            if (rvalid && best.lidx != 0xffffffffu) {
+                const unsigned fb = best.lidx / static_cast<unsigned>(fa.D);
+                const unsigned jb = best.lidx - fb * static_cast<unsigned>(fa.D);
+                const unsigned long long flat =
+                    ((c_glob * fa.F + fb) * fa.R_total + static_cast<unsigned long long>(r_glob)) * fa.D + jb;
+                peak_publish(fa.slots + r_local, best.re, best.im, flat);
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_BN));
+    }
+}
+
+inline size_t tc2_smem_bytes(int terms) {
+    const size_t stages = terms == 3 ? static_cast<size_t>(tc2_stages<3>()) * tc2_stage_bytes<3>()
+                                     : static_cast<size_t>(tc2_stages<1>()) * tc2_stage_bytes<1>();
+    return 1024 + stages + 8 * (2 * 6 + 4) + 16;
+}
+
 // H_f(m) = exp(+j 4pi/lambda * kappa * sum_axes val * t^ord) for every fine
 // cell f (mixed radix over the fine axes, last fastest), phase in FP64 cycles.
 __global__ void build_htab_kernel(TcArgs a, float2* htab) {
