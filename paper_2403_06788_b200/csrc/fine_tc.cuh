@@ -483,8 +483,10 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Arrive on a (possibly peer) CTA's barrier.  Writers of async-proxy
+// operands precede this with fence.proxy.async, as CUTLASS does.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 __device__ __noinline__ void mbar_wait_cluster_slow(uint32_t bar, uint32_t parity) {
@@ -663,21 +665,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             for (int kb = 0; kb < nkb; ++kb, ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
+                const int mf = kb * (TC_BK / 2) + 4 * c;
+                // operand inputs do not depend on the stage: load them before waiting
+                float4 hA[2], hB[2];
+                float2 w0[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    hA[u] = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf));
+                    hB[u] = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf + 2));
+                    w0[u] = wpow(dq[u] * mf, M);
+                }
                 mbar_wait(empty0 + 8 * s, ph ^ 1);
                 uint8_t* g_hi = smem + s * SB + PLANES * TC2_X_BYTES;
                 uint8_t* g_lo = g_hi + TC2_G_BYTES;
-                const int mf = kb * (TC_BK / 2) + 4 * c;
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     const int L0 = 2 * ((lane & 3) + 4 * wg + 32 * u), L1 = L0 + 1;
                     const uint32_t o0 = (L0 >> 3) * 1024 + (L0 & 7) * 128 + ((c ^ (L0 & 7)) << 4);
                     const uint32_t o1 = (L1 >> 3) * 1024 + (L1 & 7) * 128 + ((c ^ (L1 & 7)) << 4);
                     uint32_t h0[4], h1[4], l0[4], l1[4];
-                    float2 wv = wpow(dq[u] * mf, M);
-                    const float4 hA = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf));
-                    const float4 hB = __ldg(reinterpret_cast<const float4*>(Hq[u] + mf + 2));
-                    const float2 hv[4] = {make_float2(hA.x, hA.y), make_float2(hA.z, hA.w),
-                                          make_float2(hB.x, hB.y), make_float2(hB.z, hB.w)};
+                    float2 wv = w0[u];
+                    const float2 hv[4] = {make_float2(hA[u].x, hA[u].y), make_float2(hA[u].z, hA[u].w),
+                                          make_float2(hB[u].x, hB[u].y), make_float2(hB[u].z, hB[u].w)};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         float2 b = cmul(hv[e], wv);
