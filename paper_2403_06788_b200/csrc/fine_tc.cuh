@@ -829,9 +829,13 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
         if (M < 32) throw std::invalid_argument("ltci_cuda: tcgen05 fine path needs M >= 32");
         return true;
     }
-    // AUTO: the CUDA-core FFT path up to M = 1024 (measured faster than the
-    // 3-term tensor path at C1); beyond it the tensor path.
-    return M > 1024;
+    // AUTO (by measurement): the 3-term (FP32-class) tensor path
+    // for Doppler-windowed DS-GRFT (C1: 252 ms vs 302 ms FFT; C4: 12.3 vs
+    // 16.7 ms/CPI) and whenever M > 1024; the CUDA-core FFT path for the full
+    // Doppler axis (DS-KT-MFP, D = M, where the dense form is ~8x the work)
+    // and small M.
+    if (keep_dense) return M > 1024;
+    return M > 1024 || (M >= 64 && 2 * D <= M);
 }
 
 inline size_t tc_smem_bytes(int terms, int M) {
