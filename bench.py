@@ -331,10 +331,8 @@ def main():
         hbm = peaks_json.get("hbm_gbs", 6650.0)
         x_bytes = 8.0 * coarse * rows_here * p.M + 8.0 * p.K * p.M
         coarse_gbs = x_bytes / (st["coarse_ms"] * 1e-3) / 1e9 if st["coarse_ms"] > 0 else None
-        D_here = D
-        use_tc = args.fine_path in ("tc", "tcfast") or (
-            args.fine_path == "auto" and (p.M > 1024 or (p.M >= 64 and 2 * D_here <= p.M)))
-        terms = 1 if args.fine_path == "tcfast" else 3
+        path_id, terms = eng.fine_path()  # what the engine actually runs
+        use_tc = path_id in (A.FINE_TC_DENSE, A.FINE_TC_FAST)
         fine_s = st["fine_ms"] * 1e-3
         if use_tc:
             peak_tc = peaks_json.get("bf16_tflops", 1649.5)

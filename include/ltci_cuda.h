@@ -195,6 +195,9 @@ int ltci_engine_peaks_device(ltci_engine *e, void **d_ptr, int32_t *n_rows);
 int ltci_engine_stats(ltci_engine *e, int64_t *launches, double *fine_ms, double *coarse_ms,
                       double *keystone_ms);
 int ltci_engine_set_timing(ltci_engine *e, int enable);
+/* Fine-stage formulation this engine runs (LTCI_FINE_FFT_CUDA_CORE or
+ * LTCI_FINE_TC_DENSE / LTCI_FINE_TC_FAST) and its fp16 split terms (0 for FFT). */
+int ltci_engine_fine_path(ltci_engine *e, int32_t *path, int32_t *terms);
 /* hypotheses (cells) and integrations covered by this engine's row slice */
 int ltci_engine_work(ltci_engine *e, uint64_t *hypotheses, uint64_t *integrations);
 

@@ -20,7 +20,8 @@ EXPORTS = (
     "ltci_cuda_ds_grft", "ltci_cuda_ds_kt_mfp", "ltci_cuda_free_map", "ltci_cuda_keystone",
     "ltci_cuda_mgift", "ltci_cuda_gft", "ltci_cuda_detection_threshold", "ltci_engine_create",
     "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
-    "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_work",
+    "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path",
+    "ltci_engine_work",
     "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
 )
 
@@ -79,6 +80,7 @@ def load():
     lib.ltci_engine_stats.argtypes = [vp, P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_double)]
     lib.ltci_engine_set_timing.argtypes = [vp, C.c_int]
     lib.ltci_engine_work.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
+    lib.ltci_engine_fine_path.argtypes = [vp, P(C.c_int32), P(C.c_int32)]
     lib.ltci_cuda_measure_fp32_peak.argtypes = [C.c_int, P(C.c_double)]
     lib.ltci_cuda_last_error.restype = C.c_char_p
     lib.ltci_cuda_version.restype = C.c_int

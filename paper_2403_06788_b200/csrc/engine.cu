@@ -1204,6 +1204,14 @@ int ltci_engine_set_timing(ltci_engine* e, int enable) {
     });
 }
 
+int ltci_engine_fine_path(ltci_engine* e, int32_t* path, int32_t* terms) {
+    return guarded([&] {
+        if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        if (path) *path = e->use_tc ? (e->tc_terms == 1 ? LTCI_FINE_TC_FAST : LTCI_FINE_TC_DENSE) : LTCI_FINE_FFT_CUDA_CORE;
+        if (terms) *terms = e->use_tc ? e->tc_terms : 0;
+    });
+}
+
 int ltci_engine_work(ltci_engine* e, uint64_t* hypotheses, uint64_t* integrations) {
     return guarded([&] {
         if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");

@@ -834,8 +834,9 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
     // 16.7 ms/CPI) and whenever M > 1024; the CUDA-core FFT path for the full
     // Doppler axis (DS-KT-MFP, D = M, where the dense form is ~8x the work)
     // and small M.
+    // (C0, M = 256, D = 151: 0.68 vs 1.25 ms; C3 KT, D = M = 1024: FFT ~4x faster)
     if (keep_dense) return M > 1024;
-    return M > 1024 || (M >= 64 && 2 * D <= M);
+    return M > 1024 || (M >= 64 && (D <= 160 || 2 * D <= M));
 }
 
 inline size_t tc_smem_bytes(int terms, int M) {

@@ -167,6 +167,12 @@ class Engine:
                        self._lib)
         return {"launches": n.value, "fine_ms": f.value, "coarse_ms": c.value, "keystone_ms": k.value}
 
+    def fine_path(self):
+        """(path, terms): the fine-stage formulation this engine runs."""
+        pth, t = C.c_int32(), C.c_int32()
+        _lib.raise_for(self._lib.ltci_engine_fine_path(self._h, C.byref(pth), C.byref(t)), self._lib)
+        return pth.value, t.value
+
     def work(self):
         h, i = C.c_uint64(), C.c_uint64()
         _lib.raise_for(self._lib.ltci_engine_work(self._h, C.byref(h), C.byref(i)), self._lib)
