@@ -829,6 +829,7 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
         if (M < 32) throw std::invalid_argument("ltci_cuda: tcgen05 fine path needs M >= 32");
         return true;
     }
+    if (fine_path == 1) return false;  // explicit CUDA-core FFT path
     // AUTO (by measurement): the 3-term (FP32-class) tensor path
     // for Doppler-windowed DS-GRFT (C1: 252 ms vs 302 ms FFT; C4: 12.3 vs
     // 16.7 ms/CPI) and whenever M > 1024; the CUDA-core FFT path for the full

@@ -89,3 +89,18 @@ def test_tc_fast_within_contract():
     rel = np.abs(np.abs(gm.peak_value) - np.abs(g["peak_value"])) / ref_max
     assert rel.max() <= TOL
     assert abs(abs(gm.argmax_value) - ref_max) <= TOL * ref_max
+
+
+def test_fine_path_selection_is_honoured():
+    """Explicit FFT / tensor requests run that path; AUTO follows the measured rule."""
+    from paper_2403_06788_b200.detectors import Engine
+    w = config(0)
+    for req, want in ((A.FINE_FFT_CUDA_CORE, A.FINE_FFT_CUDA_CORE), (A.FINE_TC_DENSE, A.FINE_TC_DENSE),
+                      (A.FINE_TC_FAST, A.FINE_TC_FAST), (A.FINE_AUTO, A.FINE_TC_DENSE)):
+        e = Engine(w.params, w.space, opt=DetectorOptions(fine_path=req))
+        assert e.fine_path()[0] == want
+        e.close()
+    w3 = config(3)
+    e = Engine(w3.params, w3.space, 1, w3.amb, DetectorOptions())
+    assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE  # full Doppler axis -> FFT
+    e.close()
