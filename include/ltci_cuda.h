@@ -168,6 +168,30 @@ int ltci_cuda_gft(const double *rows, const ltci_radar *p, const double *fine_hi
 double ltci_cuda_detection_threshold(const ltci_radar *p, double sigma2, double pfa, int bins,
                                      int *status);
 
+/* ---- detection extraction (host C++, over the returned candidates) ------ */
+/* One detection: motion estimate c[0..n_coef-1] (c0 = range, c1 = velocity,
+ * c_p = order-p coefficient), statistic |Y|, flat cell index, and for
+ * DS-KT-MFP the folding factor and baseband velocity.
+ * Replaces Detection (proj/include/ltci/detection.hpp:76-82). */
+typedef struct {
+    double statistic;
+    double c[LTCI_MAX_ORDER + 1];
+    int32_t n_coef;
+    int32_t has_q;
+    int32_t q;
+    double baseband_velocity;
+    uint64_t flat_index;
+} ltci_detection;
+
+/* extract_detections (proj/src/detection.cpp:158-244): local maxima over the
+ * range / Doppler / order-2 axes among candidates above gamma, recomposed with
+ * detection_from_cell (:124-153), near-duplicates merged along the ridge,
+ * strongest first.  Writes min(n, max_out) detections, returns n in *n_out.
+ * amb may be NULL for DS-GRFT maps. */
+int ltci_cuda_extract_detections(const ltci_detection_map *map, const ltci_dual_space *space,
+                                 const ltci_ambiguity *amb, double gamma, ltci_detection *out,
+                                 int max_out, int *n_out);
+
 /* ---- engine: device-resident plan for streaming / benchmarking ---------- */
 typedef struct ltci_engine ltci_engine;
 

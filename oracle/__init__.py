@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from paper_2403_06788_b200 import _cabi as A
-from paper_2403_06788_b200.model import (AmbiguitySpace, DetectionMap, DetectorOptions, DualScaleSpace,
+from paper_2403_06788_b200.model import (AmbiguitySpace, DetectionMap, DetectorOptions, DualScaleSpace,  # noqa: F401
                                          RadarParams, map_from_c)
 
 HERE = os.path.dirname(os.path.abspath(__file__))

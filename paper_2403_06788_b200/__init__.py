@@ -8,9 +8,10 @@ with the reference's C++ detector API as the drop-in (lib/libltci_b200.so).
 from .model import (AmbiguitySpace, Bounds, DetectionMap, DetectorOptions, DualScaleSpace, Grid, RadarParams,
                     RangeRoi, StepSizes, build_ambiguity, build_dual_scale, step_sizes, split_velocity)
 from .detectors import Engine, detection_threshold, ds_grft, ds_kt_mfp, gft, keystone, mgift
+from .detection import Detection, extract_detections
 
 __all__ = [
     "AmbiguitySpace", "Bounds", "DetectionMap", "DetectorOptions", "DualScaleSpace", "Grid", "RadarParams",
     "RangeRoi", "StepSizes", "build_ambiguity", "build_dual_scale", "step_sizes", "split_velocity", "Engine",
-    "detection_threshold", "ds_grft", "ds_kt_mfp", "gft", "keystone", "mgift",
+    "detection_threshold", "ds_grft", "ds_kt_mfp", "gft", "keystone", "mgift", "Detection", "extract_detections",
 ]

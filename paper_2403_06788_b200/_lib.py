@@ -22,7 +22,7 @@ EXPORTS = (
     "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
     "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path",
     "ltci_engine_work",
-    "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
+    "ltci_cuda_extract_detections", "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
 )
 
 _lib = None

@@ -469,6 +469,8 @@ struct DevBuf {
 
 }  // namespace
 
+void ltcib_set_last_error(const char* msg) { g_err = msg ? msg : ""; }
+
 struct ltci_engine {
     Plan pl;
     int device = 0;

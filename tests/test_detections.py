@@ -1,0 +1,114 @@
+"""CPU: extract_detections / detection_from_cell (library C++, csrc/detection.cpp)
+against the reference's own extract_detections (oracle/_ref) on the same
+candidate lists (our FP64 oracle maps, so inputs are identical)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2403_06788_b200 import _cabi as A
+from paper_2403_06788_b200.configs import config
+from paper_2403_06788_b200.detection import extract_detections, _to_c
+from paper_2403_06788_b200.model import DetectorOptions
+
+from helpers import cube, load, radar, space
+
+needs_ref = pytest.mark.skipif(not O.have_ref(), reason="reference not built (oracle/_ref)")
+
+
+def _ref_extract(m, gamma):
+    lib = O.ref()
+    cm, keep = _to_c(m)
+    s = m.dual.to_c()
+    a = m.amb.to_c() if m.amb is not None else None
+    rows = np.zeros((4096, 6))
+    n = C.c_int(0)
+    rc = lib.ref_extract_ds(C.byref(cm), C.byref(s), C.byref(a) if a is not None else None, gamma, 4096,
+                            rows.ctypes.data_as(C.c_void_p), C.byref(n))
+    assert rc == 0, lib.ref_last_error()
+    return rows[: n.value]
+
+
+def _compare(dets, rows):
+    assert len(dets) == len(rows)
+    for d, r in zip(dets, rows):
+        assert d.flat_index == int(r[5])
+        assert d.statistic == pytest.approx(r[0], rel=1e-12)
+        for k, c in enumerate(d.estimate):
+            assert c == pytest.approx(r[1 + k], rel=1e-12, abs=1e-9)
+
+
+@needs_ref
+def test_extract_matches_reference_c0():
+    g = load("c0.npz")
+    w = config(0)
+    gamma = float(g["gamma"])
+    m = O.port_ds(cube(g), w.params, w.space, DetectorOptions(retain_threshold=gamma))
+    dets = extract_detections(m, gamma)
+    assert len(dets) > 5
+    _compare(dets, _ref_extract(m, gamma))
+
+
+@needs_ref
+def test_extract_matches_reference_kt_and_small():
+    for name, variant in (("small_grft.npz", 0), ("small_kt.npz", 1)):
+        g = load(name)
+        p = radar(g)
+        s = space(g, p)
+        amb = O.AmbiguitySpace(int(g["amb"][0]), int(g["amb"][1])) if variant else None
+        retain = float(g["retain"])
+        m = O.port_ds(cube(g), p, s, DetectorOptions(retain_threshold=retain), variant, amb)
+        for gamma in (retain, 2 * retain):
+            _compare(extract_detections(m, gamma), _ref_extract(m, gamma))
+
+
+def test_extract_rejects_gamma_below_retention():
+    g = load("c0.npz")
+    w = config(0)
+    m = O.port_ds(cube(g), w.params, w.space, DetectorOptions(retain_threshold=float(g["gamma"])))
+    with pytest.raises(ValueError, match="retention"):
+        extract_detections(m, float(g["gamma"]) / 2)
+    with pytest.raises(ValueError):
+        extract_detections(m, -1.0)
+
+
+def test_noiseless_c0_yields_one_detection_at_truth():
+    """proj/tests/test_detectors.cpp:285-301 analogue on the C0 target."""
+    w = config(0)
+    x = w.cube(noise=False)
+    gamma = 0.4 * w.params.M * w.params.K_valid * abs(w.targets[0][0])
+    m = O.port_ds(x, w.params, w.space, DetectorOptions(retain_threshold=gamma))
+    dets = extract_detections(m, gamma)
+    assert 1 <= len(dets) <= 8
+    d = dets[0]  # strongest first; the rest are DFM sidelobes above 0.4 of the peak
+    assert round(d.estimate[0] / w.params.delta_R()) == 200
+    assert abs(d.estimate[1] - 87.0) < 0.2 and abs(d.estimate[2] - 2.0) < 0.2
+    assert all(e.statistic <= d.statistic for e in dets)
+    if O.have_ref():
+        _compare(dets, _ref_extract(m, gamma))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fine_path", [1, 2])
+def test_gpu_map_detections(fine_path):
+    """GPU map -> native extract: identical to the reference's extract on the
+    same GPU candidates, and the same detections (flat index, statistic to TOL)
+    as the FP64 oracle map."""
+    from paper_2403_06788_b200 import ds_grft
+
+    g = load("c0.npz")
+    w = config(0)
+    gamma = float(g["gamma"])
+    gm = ds_grft(cube(g), w.params, w.space, DetectorOptions(retain_threshold=gamma, fine_path=fine_path))
+    dets = extract_detections(gm, gamma)
+    if O.have_ref():
+        _compare(dets, _ref_extract(gm, gamma))
+    om = O.port_ds(cube(g), w.params, w.space, DetectorOptions(retain_threshold=gamma))
+    odets = extract_detections(om, gamma)
+    assert [d.flat_index for d in dets] == [d.flat_index for d in odets]
+    for d, o in zip(dets, odets):
+        assert d.statistic == pytest.approx(o.statistic, rel=1e-3)
+        assert d.estimate == pytest.approx(o.estimate, rel=1e-12, abs=1e-9)
