@@ -52,7 +52,8 @@ enum {
     LTCI_CONDITION_VIOLATED = 2, /* ltci::ConditionViolated        */
     LTCI_RUNTIME_ERROR = 3,    /* std::runtime_error (CUDA failure) */
     LTCI_BAD_ALLOC = 4,        /* std::bad_alloc (result too large) */
-    LTCI_NO_DEVICE = 5         /* no CUDA device / extension missing */
+    LTCI_NO_DEVICE = 5,        /* no CUDA device / extension missing */
+    LTCI_IO_ERROR = 6          /* ltci::IoError (cube file container) */
 };
 
 /* detector kinds, same order as ltci::DetectorKind (detection.hpp:12) */
@@ -224,6 +225,35 @@ int ltci_engine_set_timing(ltci_engine *e, int enable);
 int ltci_engine_fine_path(ltci_engine *e, int32_t *path, int32_t *terms);
 /* hypotheses (cells) and integrations covered by this engine's row slice */
 int ltci_engine_work(ltci_engine *e, uint64_t *hypotheses, uint64_t *integrations);
+
+/* ---- cube file container ------------------------
+ * The reference's "LTCI" little-endian container (proj/include/ltci/cube_io.hpp:
+ * 9-14): magic, version u32 = 1, domain u8 (0 freq-pulse, 1 range-pulse),
+ * K, M, K_valid u32, fc, fs, Br, PRF, sigma2 f64 (61-byte header), then K*M
+ * complex samples as (re, im) f64 pairs, pulse-major.  Errors mirror
+ * ltci::IoError (LTCI_IO_ERROR) with the reference's messages. */
+typedef struct {
+    int32_t domain;     /* 0 = freq-pulse, 1 = range-pulse */
+    ltci_radar radar;   /* rebuilt with RadarParams::create semantics */
+    double sigma2;
+} ltci_cube_header;
+
+/* header only (read_cube_file's checks on the first 61 bytes and the
+ * payload length / trailing bytes; proj/src/cube_io.cpp:121-170) */
+int ltci_cuda_cube_file_info(const char *path, ltci_cube_header *out);
+/* read_cube_file (proj/src/cube_io.cpp:121-179): payload into a host buffer of
+ * 2*K*M doubles (capacity checked) */
+int ltci_cuda_cube_file_read(const char *path, ltci_cube_header *hdr, double *out, uint64_t capacity_doubles);
+/* write_cube_file (proj/src/cube_io.cpp:66-119): temp file + rename */
+int ltci_cuda_cube_file_write(const char *path, const ltci_cube_header *hdr, const double *data);
+/* The wire path: stream a freq-pulse cube file through pinned staging buffers
+ * straight into the engine's device echo (chunked fread overlapped with async
+ * H2D, f64 -> c64 on the device), then run.  Replaces read_cube_file +
+ * CubeFile::to_freq_cube + ds_grft/ds_kt_mfp (proj/tools/ltci_main.cpp:67-137).
+ * The file's radar must equal the engine's (reference: radar mismatch ->
+ * invalid_argument); a range-pulse file is ConditionViolated as in
+ * CubeFile::to_freq_cube (proj/src/cube_io.cpp:48-52). */
+int ltci_engine_run_file(ltci_engine *e, const char *path, void *stream);
 
 /* Roofline denominator for the CUDA-core fine path: dense FP32 FFMA issue
  * rate of this device, measured with a register-resident FMA chain kernel

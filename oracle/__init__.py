@@ -94,6 +94,8 @@ def ref():
         lib.ref_extract_ds.argtypes = [P(A.CDetectionMap), P(A.CDualSpace), P(A.CAmbiguity), C.c_double, C.c_int,
                                        vp, P(C.c_int)]
         lib.ref_resolve_threads.argtypes = [C.c_int]
+        lib.ref_write_cube_file.argtypes = [C.c_char_p, P(A.CCubeHeader), vp]
+        lib.ref_read_cube_file.argtypes = [C.c_char_p, P(A.CCubeHeader), vp, C.c_uint64]
         _ref = lib
     return _ref
 
@@ -282,3 +284,21 @@ def ref_point(cube, params, ctilde, range_bin):
     r = params.to_c()
     _check(lib.ref_fd_grft_point(_vp(data), C.byref(r), arr, len(ctilde), range_bin, _vp(out)), lib)
     return complex(out[0], out[1])
+
+
+# ------------------------------------------------- cube file (reference) ---
+def ref_write_cube_file(path, params, cube, sigma2=0.0, domain=0):
+    lib = ref()
+    data = _c128(cube)
+    h = A.CCubeHeader(domain, params.to_c(), sigma2)
+    _check(lib.ref_write_cube_file(str(path).encode(), C.byref(h), _vp(data)), lib)
+
+
+def ref_read_cube_file(path, max_samples=1 << 24):
+    """(domain, params, sigma2, complex (M, K) data) via ltci::read_cube_file."""
+    lib = ref()
+    out = np.empty(max_samples, np.complex128)
+    h = A.CCubeHeader()
+    _check(lib.ref_read_cube_file(str(path).encode(), C.byref(h), _vp(out), 2 * out.size), lib)
+    p = RadarParams.from_c(h.radar)
+    return int(h.domain), p, float(h.sigma2), out[: p.K * p.M].reshape(p.M, p.K).copy()

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "ltci/bench.hpp"
+#include "ltci/cube_io.hpp"
 #include "ltci/detection.hpp"
 #include "ltci/detectors.hpp"
 #include "ltci/parallel.hpp"
@@ -46,6 +47,8 @@ int guarded(F&& f) {
         return LTCI_OK;
     } catch (const R::ConditionViolated& e) {
         return fail(LTCI_CONDITION_VIOLATED, e.what());
+    } catch (const R::IoError& e) {
+        return fail(LTCI_IO_ERROR, e.what());
     } catch (const std::invalid_argument& e) {
         return fail(LTCI_INVALID_ARGUMENT, e.what());
     } catch (const std::bad_alloc& e) {
@@ -471,6 +474,32 @@ int ref_extract_ds(const ltci_detection_map* m, const ltci_dual_space* s, const 
             row[5] = static_cast<double>(map.encode(dets[i].cell));
         }
         *n_out = static_cast<int>(dets.size());
+    });
+}
+
+// write_cube_file (proj/src/cube_io.cpp:66-119) of a CubeFile built field by field
+int ref_write_cube_file(const char* path, const ltci_cube_header* h, const double* data) {
+    return guarded([&] {
+        R::CubeFile f;
+        f.domain = static_cast<std::uint8_t>(h->domain);
+        f.params = radar_of(h->radar);
+        f.sigma2 = h->sigma2;
+        const std::size_t n = static_cast<std::size_t>(h->radar.K) * h->radar.M;
+        f.data.resize(n);
+        for (std::size_t i = 0; i < n; ++i) f.data[i] = R::cplx(data[2 * i], data[2 * i + 1]);
+        R::write_cube_file(path, f);
+    });
+}
+
+// read_cube_file (proj/src/cube_io.cpp:121-179)
+int ref_read_cube_file(const char* path, ltci_cube_header* h, double* out, uint64_t cap) {
+    return guarded([&] {
+        R::CubeFile f = R::read_cube_file(path);
+        h->domain = f.domain;
+        radar_to(f.params, &h->radar);
+        h->sigma2 = f.sigma2;
+        if (cap < 2 * f.data.size()) throw std::invalid_argument("ref_read_cube_file: buffer too small");
+        copy_out(f.data, out);
     });
 }
 

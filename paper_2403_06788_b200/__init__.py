@@ -9,9 +9,11 @@ from .model import (AmbiguitySpace, Bounds, DetectionMap, DetectorOptions, DualS
                     RangeRoi, StepSizes, build_ambiguity, build_dual_scale, step_sizes, split_velocity)
 from .detectors import Engine, detection_threshold, ds_grft, ds_kt_mfp, gft, keystone, mgift
 from .detection import Detection, extract_detections
+from .cube_io import CubeFile, cube_file_info, read_cube_file, write_cube_file
 
 __all__ = [
     "AmbiguitySpace", "Bounds", "DetectionMap", "DetectorOptions", "DualScaleSpace", "Grid", "RadarParams",
     "RangeRoi", "StepSizes", "build_ambiguity", "build_dual_scale", "step_sizes", "split_velocity", "Engine",
     "detection_threshold", "ds_grft", "ds_kt_mfp", "gft", "keystone", "mgift", "Detection", "extract_detections",
+    "CubeFile", "cube_file_info", "read_cube_file", "write_cube_file",
 ]

@@ -10,7 +10,7 @@ import ctypes as C
 MAX_ORDER = 4
 MAX_AXES = 8
 
-OK, INVALID_ARGUMENT, CONDITION_VIOLATED, RUNTIME_ERROR, BAD_ALLOC, NO_DEVICE = range(6)
+OK, INVALID_ARGUMENT, CONDITION_VIOLATED, RUNTIME_ERROR, BAD_ALLOC, NO_DEVICE, IO_ERROR = range(7)
 FD_GRFT, TD_GRFT, KT_MFP, DS_GRFT, DS_KT_MFP = range(5)
 AXIS_RANGE, AXIS_VELOCITY, AXIS_HIGHER, AXIS_DOPPLER, AXIS_COARSE, AXIS_FINE, AXIS_FOLDING = range(7)
 VARIANT_GRFT, VARIANT_KTMFP = 0, 1
@@ -60,3 +60,13 @@ class CDetectionMap(C.Structure):
 
 
 PMap = C.POINTER(CDetectionMap)
+
+
+class CDetection(C.Structure):
+    _fields_ = [("statistic", C.c_double), ("c", C.c_double * (MAX_ORDER + 1)), ("n_coef", C.c_int32),
+                ("has_q", C.c_int32), ("q", C.c_int32), ("baseband_velocity", C.c_double),
+                ("flat_index", C.c_uint64)]
+
+
+class CCubeHeader(C.Structure):
+    _fields_ = [("domain", C.c_int32), ("radar", CRadar), ("sigma2", C.c_double)]

@@ -21,8 +21,9 @@ EXPORTS = (
     "ltci_cuda_mgift", "ltci_cuda_gft", "ltci_cuda_detection_threshold", "ltci_engine_create",
     "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
     "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path",
-    "ltci_engine_work",
-    "ltci_cuda_extract_detections", "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
+    "ltci_engine_work", "ltci_engine_run_file",
+    "ltci_cuda_extract_detections", "ltci_cuda_cube_file_info", "ltci_cuda_cube_file_read",
+    "ltci_cuda_cube_file_write", "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
 )
 
 _lib = None
@@ -36,6 +37,10 @@ class ConditionViolated(LtciError):
     """Mirror of ltci::ConditionViolated (proj/include/ltci/common.hpp:17-20)."""
 
 
+class IoError(LtciError):
+    """Mirror of ltci::IoError (proj/include/ltci/common.hpp:36-39)."""
+
+
 def raise_for(rc: int, lib) -> None:
     if rc == A.OK:
         return
@@ -46,6 +51,8 @@ def raise_for(rc: int, lib) -> None:
         raise ConditionViolated(msg)
     if rc == A.BAD_ALLOC:
         raise MemoryError(msg)  # std::bad_alloc
+    if rc == A.IO_ERROR:
+        raise IoError(msg)
     raise LtciError(msg)
 
 
@@ -82,6 +89,12 @@ def load():
     lib.ltci_engine_work.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     lib.ltci_engine_fine_path.argtypes = [vp, P(C.c_int32), P(C.c_int32)]
     lib.ltci_cuda_measure_fp32_peak.argtypes = [C.c_int, P(C.c_double)]
+    lib.ltci_cuda_extract_detections.argtypes = [P(A.CDetectionMap), P(A.CDualSpace), P(A.CAmbiguity), C.c_double,
+                                                 P(A.CDetection), C.c_int, P(C.c_int)]
+    lib.ltci_cuda_cube_file_info.argtypes = [C.c_char_p, P(A.CCubeHeader)]
+    lib.ltci_cuda_cube_file_read.argtypes = [C.c_char_p, P(A.CCubeHeader), vp, C.c_uint64]
+    lib.ltci_cuda_cube_file_write.argtypes = [C.c_char_p, P(A.CCubeHeader), vp]
+    lib.ltci_engine_run_file.argtypes = [vp, C.c_char_p, vp]
     lib.ltci_cuda_last_error.restype = C.c_char_p
     lib.ltci_cuda_version.restype = C.c_int
     _lib = lib

@@ -21,6 +21,7 @@
 
 #include "../../include/ltci_cuda.h"
 #include "coarse.cuh"
+#include "cube_io.hpp"
 #include "fine_fft.cuh"
 #include "fine_tc.cuh"
 
@@ -55,6 +56,9 @@ int guarded(F&& f) {
         return LTCI_OK;
     } catch (const Error& e) {
         g_err = e.msg;
+        return e.code;
+    } catch (const ltcib::CubeError& e) {
+        g_err = e.what();
         return e.code;
     } catch (const std::bad_alloc& e) {
         g_err = std::string("allocation failed: ") + e.what();
@@ -496,6 +500,10 @@ struct ltci_engine {
     DevBuf<float2> htab;
     bool htab_ready = false;
     CUtensorMap tm_hi{}, tm_lo{};
+    // cube-file wire path: two pinned staging blocks, reused across runs
+    double* stage[2] = {nullptr, nullptr};
+    size_t stage_doubles = 0;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -1151,6 +1159,10 @@ void ltci_engine_destroy(ltci_engine* e) {
         DeviceGuard dg(e->device);
         for (auto& x : e->ev) cudaEventDestroy(x);
         e->ev.clear();
+        for (int i = 0; i < 2; ++i) {
+            if (e->stage[i]) cudaFreeHost(e->stage[i]);
+            if (e->stage_ev[i]) cudaEventDestroy(e->stage_ev[i]);
+        }
         delete e;
     }
 }
@@ -1168,6 +1180,48 @@ int ltci_engine_run_host(ltci_engine* e, const double* cube, void* stream) {
         DeviceGuard dg(e->device);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         upload_host_cube(e, cube, st);
+        run_device_impl(e, e->cube_c64.p, st);
+        e->launches += 1;  // conversion kernel
+    });
+}
+
+// The wire path: file -> two pinned staging blocks ->
+// async H2D into the f64 echo buffer, the fread of block i+1 overlapping the
+// DMA of block i; then f64 -> c64 on the device and the detector run.
+int ltci_engine_run_file(ltci_engine* e, const char* path, void* stream) {
+    return guarded([&] {
+        if (!e || !path) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        ltcib::CubeReader rd;
+        rd.open(path);
+        if (rd.h.domain != 0)  // CubeFile::to_freq_cube (proj/src/cube_io.cpp:48-52)
+            fail(LTCI_CONDITION_VIOLATED, "cube file holds range-pulse data, not freq-pulse");
+        check_same_params(rd.h.radar, e->pl.rp);
+        DeviceGuard dg(e->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t n = static_cast<size_t>(e->pl.rp.K) * e->pl.rp.M;
+        e->cube_f64.ensure(n);
+        e->cube_c64.ensure(n);
+        const size_t block = 4u << 20;  // doubles per staging block (32 MiB)
+        if (!e->stage[0]) {
+            for (int i = 0; i < 2; ++i) {
+                CK(cudaHostAlloc(reinterpret_cast<void**>(&e->stage[i]), block * sizeof(double), cudaHostAllocDefault));
+                CK(cudaEventCreateWithFlags(&e->stage_ev[i], cudaEventDisableTiming));
+            }
+            e->stage_doubles = block;
+        }
+        double* dst = reinterpret_cast<double*>(e->cube_f64.p);
+        const size_t total = 2 * n;
+        int b = 0;
+        for (size_t off = 0, i = 0; off < total; off += e->stage_doubles, ++i, b ^= 1) {
+            const size_t m = std::min(e->stage_doubles, total - off);
+            if (i >= 2) CK(cudaEventSynchronize(e->stage_ev[b]));  // block b's previous DMA done
+            rd.read(e->stage[b], m);
+            CK(cudaMemcpyAsync(dst + off, e->stage[b], m * sizeof(double), cudaMemcpyHostToDevice, st));
+            CK(cudaEventRecord(e->stage_ev[b], st));
+        }
+        const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8));
+        f64_to_c64_kernel<<<blocks, 256, 0, st>>>(e->cube_f64.p, e->cube_c64.p, n);
+        CK(cudaGetLastError());
         run_device_impl(e, e->cube_c64.p, st);
         e->launches += 1;  // conversion kernel
     });

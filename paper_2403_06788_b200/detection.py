@@ -19,12 +19,6 @@ from . import _lib
 from .model import DetectionMap
 
 
-class CDetection(C.Structure):
-    _fields_ = [("statistic", C.c_double), ("c", C.c_double * (A.MAX_ORDER + 1)), ("n_coef", C.c_int32),
-                ("has_q", C.c_int32), ("q", C.c_int32), ("baseband_velocity", C.c_double),
-                ("flat_index", C.c_uint64)]
-
-
 @dataclass
 class Detection:
     estimate: List[float] = field(default_factory=list)  # c0 (range) .. cP
@@ -53,21 +47,16 @@ def _to_c(m: DetectionMap):
 
 def extract_detections(m: DetectionMap, gamma: float) -> List[Detection]:
     lib = _lib.load()
-    if not hasattr(lib, "_extract_ready"):
-        lib.ltci_cuda_extract_detections.argtypes = [C.POINTER(A.CDetectionMap), C.POINTER(A.CDualSpace),
-                                                     C.POINTER(A.CAmbiguity), C.c_double, C.POINTER(CDetection),
-                                                     C.c_int, C.POINTER(C.c_int)]
-        lib._extract_ready = True
     cm, keep = _to_c(m)
     s = m.dual.to_c()
     a = m.amb.to_c() if m.amb is not None else None
     cap = max(16, min(int(m.cand_index.size), 1 << 20))
-    out = (CDetection * cap)()
+    out = (A.CDetection * cap)()
     n = C.c_int(0)
     _lib.raise_for(lib.ltci_cuda_extract_detections(C.byref(cm), C.byref(s), C.byref(a) if a is not None else None,
                                                     gamma, out, cap, C.byref(n)), lib)
     if n.value > cap:
-        out = (CDetection * n.value)()
+        out = (A.CDetection * n.value)()
         _lib.raise_for(lib.ltci_cuda_extract_detections(C.byref(cm), C.byref(s),
                                                         C.byref(a) if a is not None else None, gamma, out,
                                                         n.value, C.byref(n)), lib)

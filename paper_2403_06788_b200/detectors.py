@@ -148,6 +148,10 @@ class Engine:
         _lib.raise_for(self._lib.ltci_engine_run_host(self._h, C.c_void_p(host_ptr), C.c_void_p(stream)),
                        self._lib)
 
+    def run_file(self, path: str, stream: int = 0):
+        """Stream an "LTCI" freq-pulse cube file into the device and run (the wire path)."""
+        _lib.raise_for(self._lib.ltci_engine_run_file(self._h, str(path).encode(), C.c_void_p(stream)), self._lib)
+
     def result(self, stream: int = 0) -> DetectionMap:
         pm = A.PMap()
         _lib.raise_for(self._lib.ltci_engine_result(self._h, C.c_void_p(stream), C.byref(pm)), self._lib)
