@@ -39,37 +39,42 @@ struct CoarseArgs {
     int radix[8];
 };
 
-__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
 
+// One CTA = PG pulses x one coarse cell, PG * K = kCoarseSamples (PG = 8 at
+// K = 2048, so an fp16 output row segment is one full 32-byte sector).
+// The K-point transform is an in-place mixed-radix decimation-in-frequency
+// FFT (radices 16, ..., 16, R_last): every butterfly reads and writes its own
+// positions, so a pass needs one barrier and only R values per thread.
+//   pass 1     global loads (all in flight) -> fractional ramp -> DFT16 ->
+//              twiddle -> shared
+//   middle     shared -> DFT16 -> twiddle -> shared (same positions)
+//   last       shared -> per-pulse rotation -> DFT_R -> preDFM -> global
+// The last pass produces, per (pulse p, row group g), the R rows g + G t
+// (G = K / R) directly: the integer part of the pulse's shift becomes a
+// rotation of the output index, folded into an input pre-twiddle, so lanes
+// p = 0..PG-1 of a warp write the same row (PG contiguous pulses).
+constexpr int kCoarseThreads = 512;
+constexpr int kCoarseSamples = 16384;
+
+__host__ __device__ constexpr int coarse_pg_for(int K, int M) {
+    return (kCoarseSamples / K) < M ? (kCoarseSamples / K) : M;
+}
+// 8 float2 of padding per 128 (2-way worst case in the middle passes; keeps
+// 8-element runs 16-byte aligned), plus 4 float2 per pulse buffer
+__host__ __device__ constexpr int cpad(int i) { return i + ((i >> 7) << 3); }
+__host__ __device__ constexpr int coarse_kp(int K) { return cpad(K) + 4; }
+
+// v[r] *= (e^{+j 2 pi num / den})^r, r = 1 .. R-1
 template <int R>
-__device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, float2* __restrict__ out,
-                                              int N, int Ns, int nfft, int stride, int tid,
-                                              int nthr) {
-    const int NR = N / R;
-    for (int idx = tid; idx < nfft * NR; idx += nthr) {
-        const int p = idx / NR;
-        const int j = idx - p * NR;
-        const float2* a = in + p * stride;
-        float2* b = out + p * stride;
-        float2 v[R];
+__device__ __forceinline__ void twiddle_pow(float2 (&v)[R], int num, int den) {
+    float s, c;
+    __sincosf(6.28318530717958647692f * static_cast<float>(num) / static_cast<float>(den), &s, &c);
+    const float2 w1 = make_float2(c, s);
+    float2 w = w1;
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = a[padi(j + r * NR)];
-        const int k = j & (Ns - 1);
-        if (Ns > 1) {
-            float s, c;
-            __sincosf(6.28318530717958647692f * static_cast<float>(k) / static_cast<float>(Ns * R), &s, &c);
-            const float2 w1 = make_float2(c, s);
-            float2 w = w1;
-#pragma unroll
-            for (int r = 1; r < R; ++r) {
-                v[r] = cmul(v[r], w);
-                w = cmul(w, w1);
-            }
-        }
-        dft_reg<R>(v);
-        const int base = (j - k) * R + k;
-#pragma unroll
-        for (int r = 0; r < R; ++r) b[padi(base + r * Ns)] = v[r];
+    for (int r = 1; r < R; ++r) {
+        v[r] = cmul(v[r], w);
+        w = cmul(w, w1);
     }
 }
 
@@ -83,25 +88,117 @@ __device__ __forceinline__ float fp16_prescale(const unsigned* maxbits, int K) {
     return ldexpf(1.0f, max(-60, min(60, e)));
 }
 
-// grid: (M / PG, c_count); block 256
-template <int PG, int OUT16>
-__global__ void __launch_bounds__(256) coarse_rm_kernel(CoarseArgs a) {
+// compile-time radix plan for K = 16^a * rem: passes 16, ..., 16, last
+__host__ __device__ constexpr int coarse_npass(int K) { return K <= 16 ? 1 : 1 + coarse_npass(K / 16); }
+__host__ __device__ constexpr int coarse_last_radix(int K) { return K <= 16 ? K : coarse_last_radix(K / 16); }
+
+// bin residue kl (mod K / R_last) -> its position after the DIF passes
+// (mixed-radix digit reversal over the radix-16 passes)
+template <int K, int NREV>
+__device__ __forceinline__ int coarse_digit_rev(int kl) {
+    int pos = 0, span = K;
+#pragma unroll
+    for (int s = 0; s < NREV; ++s) {
+        span /= 16;
+        pos += (kl & 15) * span;
+        kl >>= 4;
+    }
+    return pos;
+}
+
+template <int K, int R, int OUT16>
+__device__ __forceinline__ void coarse_last_pass(const CoarseArgs& a, const float2* __restrict__ buf, int PG,
+                                                 int lg_pg, const int* s_shift, const float2* s_pre, float sc,
+                                                 int tid) {
+    constexpr int Kp = coarse_kp(K);
+    constexpr int G = K / R;
+    constexpr int NREV = R == 1 ? coarse_npass(K) : coarse_npass(K) - 1;  // R == 1: K = 16, one pass
+    const int total = PG * G;
+    const size_t cbase = static_cast<size_t>(blockIdx.y) * a.R_slice * a.M;
+    const int m0 = blockIdx.x * PG;
+    for (int idx = tid; idx < total; idx += kCoarseThreads) {
+        const int p = idx & (PG - 1);  // lanes run over pulses first: one row per PG lanes
+        const int g = idx >> lg_pg;
+        const int A = g + a.n_base + s_shift[p];
+        const int kl = A & (G - 1);
+        const int c = (A / G) & (R - 1);
+        const int pos0 = coarse_digit_rev<K, NREV>(kl);
+        const float2* src = buf + p * Kp;
+        float2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = src[cpad(pos0 + r)];
+        // output t <- bin kl + G (t + c): pre-twiddle by w_R^{c r}, times preDFM
+        if constexpr (R > 1) twiddle_pow<R>(v, c, R);
+        const float2 pre = make_float2(s_pre[p].x * sc, s_pre[p].y * sc);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = cmul(v[r], pre);
+        dft_reg<R>(v);
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            const int n = g + G * t;
+            if (n < a.R_slice) {
+                const size_t o = cbase + static_cast<size_t>(n) * a.M + m0 + p;
+                if (OUT16) {
+                    // x = x_hi + x_lo in fp16 (interleaved re, im along K)
+                    __half2 hi = __floats2half2_rn(v[t].x, v[t].y);
+                    const float2 hf = __half22float2(hi);
+                    __half2 lo = __floats2half2_rn(v[t].x - hf.x, v[t].y - hf.y);
+                    a.Xh[o] = *reinterpret_cast<uint32_t*>(&hi);
+                    a.Xl[o] = *reinterpret_cast<uint32_t*>(&lo);
+                } else {
+                    a.X[o] = v[t];
+                }
+            }
+        }
+    }
+}
+
+// middle DIF passes: radix 16 within blocks of length L (K/16 >= L > R_last)
+template <int K, int L>
+__device__ __forceinline__ void coarse_middle_passes(float2* __restrict__ buf, int PG, int tid) {
+    if constexpr (L > coarse_last_radix(K)) {
+        constexpr int Kp = coarse_kp(K);
+        constexpr int S = L / 16;
+        constexpr int per = K / 16;  // butterflies per pulse
+        for (int idx = tid; idx < PG * per; idx += kCoarseThreads) {
+            const int p = idx / per;
+            const int rem = idx - p * per;
+            const int blk = rem / S;
+            const int j = rem - blk * S;
+            float2* ptr = buf + p * Kp;
+            const int base = blk * L + j;
+            float2 v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = ptr[cpad(base + r * S)];
+            dft_reg<16>(v);
+            twiddle_pow<16>(v, j, L);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) ptr[cpad(base + r * S)] = v[r];
+        }
+        __syncthreads();
+        coarse_middle_passes<K, S>(buf, PG, tid);
+    }
+}
+
+// grid: (M / PG, c_count); block kCoarseThreads; dynamic smem = coarse_smem_bytes
+template <int K, int OUT16>
+__global__ void __launch_bounds__(kCoarseThreads, 1) coarse_rm_kernel(CoarseArgs a) {
     extern __shared__ float2 smem[];
-    const int K = a.K;
-    const int Kp = K + (K >> 4);
-    float2* bufA = smem;
-    float2* bufB = smem + PG * Kp;
-    __shared__ int s_shift[PG];
-    __shared__ float s_ra[PG], s_rb[PG];
-    __shared__ float2 s_pre[PG];
+    constexpr int Kp = coarse_kp(K);
+    const int PG = coarse_pg_for(K, a.M);
+    const int lg_pg = __ffs(PG) - 1;
+    float2* buf = smem;
+    float2* s_pre = smem + PG * Kp;
+    int* s_shift = reinterpret_cast<int*>(s_pre + PG);
+    float* s_ra = reinterpret_cast<float*>(s_shift + PG);
+    float* s_rb = s_ra + PG;
 
     const int tid = threadIdx.x;
     const int m0 = blockIdx.x * PG;
-    const int c_local = blockIdx.y;
-    const unsigned long long c = a.c_begin + c_local;
+    const unsigned long long c = a.c_begin + blockIdx.y;
 
-    if (tid < PG) {
-        const int m = m0 + tid;
+    for (int q = tid; q < PG; q += kCoarseThreads) {
+        const int m = m0 + q;
         const double t = static_cast<double>(m + 1) * a.inv_prf;
         const double* cp = a.cparams + 4 * c;
         double s_rm, s_predfm, b = 0.0;
@@ -126,69 +223,70 @@ __global__ void __launch_bounds__(256) coarse_rm_kernel(CoarseArgs a) {
         const double frac = delta - sh;
         long long shl = static_cast<long long>(sh) % K;
         if (shl < 0) shl += K;
-        s_shift[tid] = static_cast<int>(shl);
-        s_ra[tid] = static_cast<float>(6.283185307179586 * frac / K);
-        s_rb[tid] = static_cast<float>(b);
+        s_shift[q] = static_cast<int>(shl);
+        s_ra[q] = static_cast<float>(6.283185307179586 * frac / K);
+        s_rb[q] = static_cast<float>(b);
         const double cyc = s_predfm * a.two_over_lambda;  // 4pi/lambda * S = 2pi * (2S/lambda)
         const double fr = cyc - rint(cyc);
         double ps, pc;
         sincospi(2.0 * fr, &ps, &pc);
-        s_pre[tid] = make_float2(static_cast<float>(pc), static_cast<float>(ps));
+        s_pre[q] = make_float2(static_cast<float>(pc), static_cast<float>(ps));
     }
     __syncthreads();
 
-    // load + fractional ramp
-    for (int idx = tid; idx < PG * K; idx += blockDim.x) {
-        const int p = idx / K;
-        const int k = idx - p * K;
-        const float2 y = a.cube[static_cast<size_t>(m0 + p) * K + k];
-        const float g = static_cast<float>(k < K / 2 ? k : k - K);
-        float s, co;
-        __sincosf(fmaf(s_rb[p] * g, g, s_ra[p] * g), &s, &co);
-        bufA[p * Kp + padi(k)] = cmul(y, make_float2(co, s));
-    }
-    __syncthreads();
-
-    float2* in = bufA;
-    float2* out = bufB;
-    int Ns = 1;
-    for (int ps = 0; ps < a.npass; ++ps) {
-        const int R = a.radix[ps];
-        switch (R) {
-            case 2: stockham_pass<2>(in, out, K, Ns, PG, Kp, tid, blockDim.x); break;
-            case 4: stockham_pass<4>(in, out, K, Ns, PG, Kp, tid, blockDim.x); break;
-            case 8: stockham_pass<8>(in, out, K, Ns, PG, Kp, tid, blockDim.x); break;
-            default: stockham_pass<16>(in, out, K, Ns, PG, Kp, tid, blockDim.x); break;
+    // pass 1: radix 16 over span S = K/16, straight from global
+    {
+        constexpr int S = K / 16;
+        const int total = PG * S;
+#pragma unroll 1
+        for (int i0 = tid; i0 < total; i0 += 2 * kCoarseThreads) {
+            float2 v[2][16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int idx = i0 + h * kCoarseThreads;
+                if (idx < total) {
+                    const int p = idx / S;
+                    const int j = idx - p * S;
+                    const float2* col = a.cube + static_cast<size_t>(m0 + p) * K + j;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) v[h][r] = __ldg(col + r * S);
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int idx = i0 + h * kCoarseThreads;
+                if (idx < total) {
+                    const int p = idx / S;
+                    const int j = idx - p * S;
+                    const float ra = s_ra[p], rb = s_rb[p];
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {
+                        const int k = j + r * S;
+                        const float gg = static_cast<float>(k < K / 2 ? k : k - K);
+                        float sn, cs;
+                        __sincosf(fmaf(rb * gg, gg, ra * gg), &sn, &cs);
+                        v[h][r] = cmul(v[h][r], make_float2(cs, sn));
+                    }
+                    dft_reg<16>(v[h]);
+                    if constexpr (S > 1) twiddle_pow<16>(v[h], j, K);
+                    float2* dst = buf + p * Kp;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) dst[cpad(j + r * S)] = v[h][r];
+                }
+            }
         }
         __syncthreads();
-        Ns *= R;
-        float2* tmp = in;
-        in = out;
-        out = tmp;
     }
+    coarse_middle_passes<K, K / 16>(buf, PG, tid);
 
-    // shifted ROI store, pulse-contiguous rows
-    const size_t cbase = static_cast<size_t>(c_local) * a.R_slice * a.M;
     const float sc = OUT16 ? fp16_prescale(a.maxbits, K) : 1.0f;
-    for (int idx = tid; idx < a.R_slice * PG; idx += blockDim.x) {
-        const int r = idx / PG;
-        const int p = idx - r * PG;
-        int n = a.n_base + r + s_shift[p];
-        n &= K - 1;
-        const float2 v = cmul(in[p * Kp + padi(n)], s_pre[p]);
-        const size_t o = cbase + static_cast<size_t>(r) * a.M + m0 + p;
-        if (OUT16) {
-            // x = x_hi + x_lo in fp16 (interleaved re, im along K)
-            const float xr = v.x * sc, xi = v.y * sc;
-            __half2 hi = __floats2half2_rn(xr, xi);
-            const float2 hf = __half22float2(hi);
-            __half2 lo = __floats2half2_rn(xr - hf.x, xi - hf.y);
-            a.Xh[o] = *reinterpret_cast<uint32_t*>(&hi);
-            a.Xl[o] = *reinterpret_cast<uint32_t*>(&lo);
-        } else {
-            a.X[o] = v;
-        }
-    }
+    constexpr int RL = K == 16 ? 1 : coarse_last_radix(K);
+    coarse_last_pass<K, RL, OUT16>(a, buf, PG, lg_pg, s_shift, s_pre, sc, tid);
+}
+
+inline size_t coarse_smem_bytes(int K, int M) {
+    const int PG = coarse_pg_for(K, M);
+    return static_cast<size_t>(PG) * coarse_kp(K) * sizeof(float2) + static_cast<size_t>(PG) * (8 + 4 + 4 + 4);
 }
 
 // f64 interleaved host layout -> complex64 device cube

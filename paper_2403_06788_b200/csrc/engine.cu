@@ -308,45 +308,44 @@ void radix_plan(int K, int* radix, int* npass) {
     *npass = n;
 }
 
-int coarse_pg(int K, int M) {
-    const int Kp = K + K / 16;
-    int pg = 1;
-    while (pg < 32 && 2 * (2 * pg) * Kp * static_cast<int>(sizeof(float2)) <= 140 * 1024) pg *= 2;
-    return std::min(pg, M);
-}
+int coarse_pg(int K, int M) { return coarse_pg_for(K, M); }
 
-template <int PG, int OUT16>
-void launch_coarse_pg(const CoarseArgs& a, cudaStream_t st) {
-    const int Kp = a.K + a.K / 16;
-    const size_t smem = 2ull * PG * Kp * sizeof(float2);
-    auto kern = coarse_rm_kernel<PG, OUT16>;
+template <int K, int OUT16>
+void launch_coarse_k(const CoarseArgs& a, cudaStream_t st) {
+    auto kern = coarse_rm_kernel<K, OUT16>;
+    const size_t smem = coarse_smem_bytes(K, a.M);
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         attr_done = true;
     }
-    dim3 grid(a.M / PG, a.c_count);
-    kern<<<grid, 256, smem, st>>>(a);
+    dim3 grid(a.M / coarse_pg_for(K, a.M), a.c_count);
+    kern<<<grid, kCoarseThreads, smem, st>>>(a);
     CK(cudaGetLastError());
 }
 
 template <int OUT16>
-void launch_coarse_out(const CoarseArgs& a, int pg, cudaStream_t st) {
-    switch (pg) {
-        case 1: launch_coarse_pg<1, OUT16>(a, st); break;
-        case 2: launch_coarse_pg<2, OUT16>(a, st); break;
-        case 4: launch_coarse_pg<4, OUT16>(a, st); break;
-        case 8: launch_coarse_pg<8, OUT16>(a, st); break;
-        case 16: launch_coarse_pg<16, OUT16>(a, st); break;
-        default: launch_coarse_pg<32, OUT16>(a, st); break;
+void launch_coarse_out(const CoarseArgs& a, cudaStream_t st) {
+    switch (a.K) {
+        case 16: launch_coarse_k<16, OUT16>(a, st); break;
+        case 32: launch_coarse_k<32, OUT16>(a, st); break;
+        case 64: launch_coarse_k<64, OUT16>(a, st); break;
+        case 128: launch_coarse_k<128, OUT16>(a, st); break;
+        case 256: launch_coarse_k<256, OUT16>(a, st); break;
+        case 512: launch_coarse_k<512, OUT16>(a, st); break;
+        case 1024: launch_coarse_k<1024, OUT16>(a, st); break;
+        case 2048: launch_coarse_k<2048, OUT16>(a, st); break;
+        case 4096: launch_coarse_k<4096, OUT16>(a, st); break;
+        case 8192: launch_coarse_k<8192, OUT16>(a, st); break;
+        default: fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: unsupported K");
     }
 }
 
-void launch_coarse(const CoarseArgs& a, int pg, cudaStream_t st, bool out16 = false) {
+void launch_coarse(const CoarseArgs& a, int /*pg*/, cudaStream_t st, bool out16 = false) {
     if (out16)
-        launch_coarse_out<1>(a, pg, st);
+        launch_coarse_out<1>(a, st);
     else
-        launch_coarse_out<0>(a, pg, st);
+        launch_coarse_out<0>(a, st);
 }
 
 // ---- tcgen05 fine path: TMA tensor maps over the fp16 X planes ----------
