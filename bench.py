@@ -35,6 +35,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    """Stage marker on stderr (stdout carries only the JSON line)."""
+    print(f"[bench {time.perf_counter() - _T0:8.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -43,7 +51,9 @@ def parse():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--fine-path", default="auto", choices=["auto", "fft", "tc", "tcfast"])
-    ap.add_argument("--pfa", type=float, default=1e-6)
+    ap.add_argument("--pfa", type=float, default=0.0,
+                    help="per-cell false-alarm rate of the retention threshold; 0 = min(1e-6, 1e5 / hypotheses), "
+                         "i.e. 1e-6 unless that would retain more than ~1e5 noise cells per CPI (C2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample length")
     ap.add_argument("--coarse-slice", type=int, default=0,
@@ -74,13 +84,20 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()  # sampling is live before the timed region starts
+            while not self.lines and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.01)
+            self.lines.clear()
         except OSError:
             self.proc = None
         return self
+
+    def count(self):
+        return len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -143,6 +160,21 @@ def cpu_reference_rate(w, seconds_target: float, threads: int):
         sl = configs.sliced(w, nv)
     else:
         sl = configs.sliced(w, min(nv, g0.count))
+    # bound the sample to ~seconds_target: the reference spends the same time per
+    # (coarse cell, ROI row) at any row count (the per-cell mgift is < 1 % of it),
+    # so large configs keep every coarse/fine cell of the slice but fewer rows
+    per_row = sl.integrations() / sl.space.roi.count()
+    rows = int(max(1, min(sl.space.roi.count(), seconds_target * 4e9 * threads / per_row)))
+    if rows < 4 and w.variant == 0 and g0.count >= threads:
+        # huge per-row work (C2): exactly one coarse cell per thread, and enough rows
+        # that the reference's per-(coarse, fine) DFM filter build stays amortised
+        sl = configs.sliced(w, threads, 1)
+        per_row = sl.integrations() / sl.space.roi.count()
+        rows = int(max(4, min(sl.space.roi.count(), seconds_target * 4e9 * threads / per_row)))
+    if rows < sl.space.roi.count():
+        from paper_2403_06788_b200.model import RangeRoi
+        sl.space.roi = RangeRoi(sl.space.roi.first, sl.space.roi.first + rows - 1)
+        sl.name += f" [{rows} ROI rows]"
     t0 = time.perf_counter()
     O.ref_ds(x, sl.params, sl.space, opt, sl.variant, sl.amb)
     dt = time.perf_counter() - t0
@@ -187,6 +219,14 @@ class _CAI:
         self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 2}
 
 
+def _ncu_traffic(config_index, kernel):
+    """DRAM bytes per launch of ``kernel`` from the committed ncu --set full capture (C1 only)."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_c1.json")
+    if config_index != 1 or not os.path.exists(path):
+        return None
+    return json.load(open(path)).get(kernel, {}).get("traffic_bytes_per_launch")
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -212,6 +252,8 @@ def main():
     p, s = w.params, w.space
     fine_path = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE,
                  "tcfast": A.FINE_TC_FAST}[args.fine_path]
+    if args.pfa <= 0:
+        args.pfa = min(1e-6, 1e5 / float(w.hypotheses()))
     gamma = detection_threshold(p, w.sigma2, args.pfa)
     opt = DetectorOptions(retain_threshold=gamma, fine_path=fine_path, device=local)
     R = s.roi.count()
@@ -224,7 +266,9 @@ def main():
         # one CPI sharded over range start cells
         lo, hi = rank * R // ws, (rank + 1) * R // ws
         my_cpis = [0]
+    log("engine")
     eng = Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi)
+    log("synthesising cubes")
     hyp, integ = eng.work()
 
     cubes = [scene.to_complex64_roundtrip(w.cube(cpi=c)) for c in my_cpis]  # (M, K): column-major K x M
@@ -252,16 +296,19 @@ def main():
                 per_cpi_peaks[i].copy_(peaks.view(torch.int32))  # keep each CPI's peak map
         gather_peaks()
 
+    log("warmup")
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize(dev)
 
+    log("timed steps")
     # ---- value: device-timed, L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     wall0 = time.perf_counter()
+    extra_steps = 0
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.zero_()
@@ -269,7 +316,14 @@ def main():
             step()
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
-    wall = time.perf_counter() - wall0
+        wall = time.perf_counter() - wall0
+        # a timed region shorter than the sampling period (C0: ms) gets its clocks
+        # from untimed repeats of the same step, stated in the JSON line
+        t1 = time.perf_counter()
+        while clk.proc and clk.count() < 3 and time.perf_counter() - t1 < 3.0:
+            step()
+            torch.cuda.synchronize(dev)
+            extra_steps += 1
     if ws > 1:
         dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in ev)
@@ -281,6 +335,7 @@ def main():
     value = total_integ * args.steps / (ms_max * 1e-3) / 1e9
     cpi_rate = cpis * args.steps / (ms_max * 1e-3)
 
+    log("kernel split")
     # ---- kernel split (timed pass) for the roofline
     eng.set_timing(True)
     flush.zero_()
@@ -289,6 +344,7 @@ def main():
     eng.set_timing(False)
     launches = st["launches"] * len(my_cpis)
 
+    log("e2e")
     # ---- e2e: public API from pinned host memory, results back to host
     hosts = [torch.from_numpy(c.view(np.float64).reshape(-1)).pin_memory() for c in cubes]
     e2e_ms = []
@@ -330,6 +386,7 @@ def main():
         rows_here = (hi - lo)
         hbm = peaks_json.get("hbm_gbs", 6650.0)
         x_bytes = 8.0 * coarse * rows_here * p.M + 8.0 * p.K * p.M
+        coarse_fft_flops = coarse * p.M * (5.0 * p.K * np.log2(p.K) + 8.0 * p.K)
         coarse_gbs = x_bytes / (st["coarse_ms"] * 1e-3) / 1e9 if st["coarse_ms"] > 0 else None
         path_id, terms = eng.fine_path()  # what the engine actually runs
         use_tc = path_id in (A.FINE_TC_DENSE, A.FINE_TC_FAST)
@@ -338,11 +395,13 @@ def main():
             peak_tc = peaks_json.get("bf16_tflops", 1649.5)
             peak_sus = peaks_json.get("bf16_tflops_sustained", 1394.2)
             achieved = 8.0 * integ / fine_s / 1e12  # algorithmic: 8 flop per integration
-            roof = {"bound": "tensor", "kernel": f"fine_tc_kernel<{terms}> (K2a+K3, tcgen05)",
+            roof = {"bound": "tensor", "kernel": f"fine_tc2_kernel<{terms}> (K2a+K3, tcgen05 cta_group::2)",
                     "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s", "frac": achieved / peak_tc,
-                    "traffic": None,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; SM clock stays at max under this kernel, "
-                                   "see clocks); frac_vs_sustained uses bf16_tflops_sustained",
+                    "traffic": _ncu_traffic(args.config, "fine_tc2_kernel<3>") if terms == 3 else None,
+                    "traffic_source": "profiles/r01_ncu_c1.json (ncu --set full, bytes per launch)",
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst, the conservative denominator: the SM "
+                                   "clock drops to the power cap under this kernel, 1.29-1.43 GHz in ncu); "
+                                   "frac_vs_sustained uses bf16_tflops_sustained",
                     "frac_vs_sustained": achieved / peak_sus,
                     "algorithmic": "8 flop per hypothesis x pulse integration (complex MAC)",
                     "executed_tflops": terms * achieved, "executed_frac": terms * achieved / peak_tc,
@@ -360,7 +419,12 @@ def main():
                      "fine_share": st["fine_ms"] / max(1e-9, st["fine_ms"] + st["coarse_ms"] + st["keystone_ms"]),
                      "coarse_stage": {"bound": "hbm", "achieved": coarse_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": coarse_gbs / hbm if coarse_gbs else None,
-                                      "algorithmic": "8 B x (K M echo + coarse x R x M X write)"}})
+                                      "algorithmic": "8 B x (K M echo + coarse x R x M X write)",
+                                      "fp32_tflops": coarse_fft_flops / (st["coarse_ms"] * 1e-3) / 1e12
+                                      if st["coarse_ms"] > 0 else None,
+                                      "fp32_algorithmic": "per (coarse cell, pulse): 5 K log2 K FFT + 8 K ramp",
+                                      "note": "exact fractional-delay gather = one K-point transform per "
+                                              "(coarse cell, pulse); issue-bound, see profiles/r01_ncu_c1.json"}})
         name = "DS-GRFT" if w.variant == 0 else "DS-KT-MFP"
         if cpis > 1:
             metric, unit, val, e2e_val = f"{name} CPIs/s ({cpis}-CPI stream)", "CPI/s", cpi_rate, \
@@ -384,11 +448,12 @@ def main():
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": int(cube.size * 16 * len(cubes)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms))},
             "gpu_launches": int(launches) * args.steps,
-            "clocks": clk.summary(),
+            "clocks": dict(clk.summary(), **({"untimed_repeat_steps_sampled": extra_steps} if extra_steps else {})),
             "wall_s_timed_region": wall,
         }
         if ws == 1 and not args.no_cpu_baseline:
             try:
+                log("cpu baseline")
                 cb = cpu_reference_rate(w, args.cpu_seconds, os.cpu_count() or 1)
             except Exception as e:  # reported, not fatal
                 cb = {"error": str(e)}

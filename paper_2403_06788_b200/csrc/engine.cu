@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/ltci_cuda.h"
 #include "coarse.cuh"
 #include "cube_io.hpp"
@@ -499,6 +501,11 @@ struct ltci_engine {
     DevBuf<float2> htab;
     bool htab_ready = false;
     CUtensorMap tm_hi{}, tm_lo{};
+    // candidate assembly on the device (radix sort by flat index + recentring)
+    DevBuf<unsigned long long> ck0, ck1;
+    DevBuf<float2> cv0, cv1;
+    DevBuf<double2> cvals;
+    DevBuf<unsigned char> csort_tmp;
     // cube-file wire path: two pinned staging blocks, reused across runs
     double* stage[2] = {nullptr, nullptr};
     size_t stage_doubles = 0;
@@ -761,6 +768,30 @@ void upload_host_cube(ltci_engine* e, const double* cube, cudaStream_t st) {
     CK(cudaGetLastError());
 }
 
+__global__ void cand_split_kernel(const CandRec* __restrict__ in, unsigned long long* __restrict__ keys,
+                                  float2* __restrict__ vals, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const CandRec r = in[i];
+        keys[i] = r.idx;
+        vals[i] = make_float2(r.re, r.im);
+    }
+}
+
+// the recentring twiddle of recenter() below, in FP64 on the device
+__global__ void cand_recenter_kernel(const unsigned long long* __restrict__ keys, const float2* __restrict__ vals,
+                                     double2* __restrict__ out, unsigned long long n, int D, int dop_first, int M) {
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const int jj = static_cast<int>(keys[i] % static_cast<unsigned long long>(D));
+        const int d = dop_first + jj - M / 2;
+        double s, c;
+        sincospi(2.0 * d / M, &s, &c);
+        const double re = vals[i].x, im = vals[i].y;
+        out[i] = make_double2(re * c - im * s, re * s + im * c);
+    }
+}
+
 // exp(+j 2pi d / M) for the flat index's Doppler bin (RangeDopplerMap recentring,
 // proj/src/transforms.cpp:197-212)
 void recenter(const Plan& pl, unsigned long long idx, float re, float im, double* out) {
@@ -816,9 +847,6 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         // peak slots -> per-row peaks + global argmax
         std::vector<PeakSlot> slots(pl.R_slice);
         CK(cudaMemcpyAsync(slots.data(), e->slots.p, slots.size() * sizeof(PeakSlot), cudaMemcpyDeviceToHost, st));
-        std::vector<CandRec> cands(count);
-        if (count)
-            CK(cudaMemcpyAsync(cands.data(), e->cand.p, count * sizeof(CandRec), cudaMemcpyDeviceToHost, st));
         std::vector<float2> dense;
         if (pl.keep_dense) {
             dense.resize(e->dense.n);
@@ -845,13 +873,36 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         out->argmax_value[0] = out->peak_value[2 * best];
         out->argmax_value[1] = out->peak_value[2 * best + 1];
 
-        std::sort(cands.begin(), cands.end(), [](const CandRec& a, const CandRec& b) { return a.idx < b.idx; });
+        // candidates: radix sort by flat index and recentre on the device, then
+        // one D2H per array straight into the map (scales to 1e8+ retained cells)
         out->n_candidates = count;
         out->cand_index = static_cast<uint64_t*>(xmalloc(count * sizeof(uint64_t)));
         out->cand_value = static_cast<double*>(xmalloc(2 * count * sizeof(double)));
-        for (unsigned long long i = 0; i < count; ++i) {
-            out->cand_index[i] = cands[i].idx;
-            recenter(pl, cands[i].idx, cands[i].re, cands[i].im, out->cand_value + 2 * i);
+        if (count) {
+            e->ck0.ensure(count);
+            e->ck1.ensure(count);
+            e->cv0.ensure(count);
+            e->cv1.ensure(count);
+            e->cvals.ensure(count);
+            const int blocks = static_cast<int>(std::min<unsigned long long>((count + 255) / 256, 148 * 8));
+            cand_split_kernel<<<blocks, 256, 0, st>>>(e->cand.p, e->ck0.p, e->cv0.p, count);
+            CK(cudaGetLastError());
+            const unsigned long long cells = static_cast<unsigned long long>(pl.coarse_cells) * pl.fine_cells *
+                                             static_cast<unsigned long long>(pl.R_total) * pl.D;
+            int end_bit = 1;
+            while (end_bit < 64 && (cells >> end_bit) != 0) ++end_bit;
+            size_t tmp = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, e->ck0.p, e->ck1.p, e->cv0.p, e->cv1.p, count, 0,
+                                               end_bit, st));
+            e->csort_tmp.ensure(tmp);
+            CK(cub::DeviceRadixSort::SortPairs(e->csort_tmp.p, tmp, e->ck0.p, e->ck1.p, e->cv0.p, e->cv1.p, count,
+                                               0, end_bit, st));
+            cand_recenter_kernel<<<blocks, 256, 0, st>>>(e->ck1.p, e->cv1.p, e->cvals.p, count, pl.D, pl.dop_first,
+                                                         pl.rp.M);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(out->cand_index, e->ck1.p, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(out->cand_value, e->cvals.p, count * sizeof(double2), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
         }
         if (pl.keep_dense) {
             out->dense_stored = 1;

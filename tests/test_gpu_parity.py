@@ -54,7 +54,7 @@ def test_keystone_matches_reference_golden():
 
 
 @pytest.mark.parametrize("M,K", [(4, 16), (8, 32), (16, 64), (32, 64), (64, 128), (128, 256), (256, 512),
-                                 (512, 1024), (1024, 2048)])
+                                 (512, 1024), (1024, 2048), (256, 4096), (16, 8192)])
 def test_transforms_all_sizes(M, K):
     p = RadarParams.create(3e9, 20e6, 18e6, 1000.0, M, K)
     x = scene.to_complex64_roundtrip(scene.add_noise(np.zeros((M, K), complex), 1.0, M + K))
