@@ -129,6 +129,8 @@ struct DetectionMap {
     int doppler_first = 0;
 };
 
+// proj/include/ltci/detectors.hpp:25-26
+DetectionMap fd_grft(const FreqPulseCube& cube, const SingleScaleSpace& space, const DetectorOptions& opt = {});
 DetectionMap ds_grft(const FreqPulseCube& cube, const DualScaleSpace& space, const DetectorOptions& opt = {});
 DetectionMap ds_kt_mfp(const FreqPulseCube& cube, const AmbiguitySpace& amb, const DualScaleSpace& space,
                        const DetectorOptions& opt = {});

@@ -107,6 +107,19 @@ typedef struct {
     int32_t q_min, q_max;
 } ltci_ambiguity;
 
+/* SingleScaleSpace (proj/include/ltci/search_space.hpp:50-58): per-order grids
+ * at the DFM step, c[p-1] for order p = 1..P, and the range ROI.  Built by
+ * build_single_scale (proj/src/search_space.cpp:69-79). */
+typedef struct {
+    ltci_radar radar;
+    int32_t order;                    /* P */
+    ltci_grid c[LTCI_MAX_ORDER];      /* index p-1 */
+    double rm_step[LTCI_MAX_ORDER];
+    double dfm_step[LTCI_MAX_ORDER];
+    double alpha[LTCI_MAX_ORDER];
+    int32_t roi_first, roi_last;      /* RangeRoi, inclusive */
+} ltci_single_space;
+
 typedef struct {
     double retain_threshold; /* keep cells with |Y| > this (strict) */
     int32_t keep_dense;
@@ -161,6 +174,14 @@ int ltci_cuda_ds_kt_mfp(const double *cube, const ltci_radar *cube_params,
 void ltci_cuda_free_map(ltci_detection_map *map);
 
 /* ---- kernel-level secondary boundary (host buffers, float64 complex) ---- */
+/* ltci::fd_grft (proj/include/ltci/detectors.hpp:25-26, proj/src/detectors.cpp:105-197):
+ * the single-scale frequency-domain GRFT, SURVEY.md §8(f) rank 2.  Same map
+ * contract as the reference (axes c_P..c_2, c_1, range; flat index
+ * cell * R + r; counters mf += K and ifft += 1 per motion cell; candidates
+ * |v| > retain sorted by index; argmax over every cell, ties to the lowest
+ * index).  Extension: an ROI outside [0, K) is LTCI_INVALID_ARGUMENT. */
+int ltci_cuda_fd_grft(const double *cube, const ltci_radar *cube_params, const ltci_single_space *space,
+                      const ltci_options *opt, ltci_detection_map **out);
 int ltci_cuda_keystone(const double *cube, const ltci_radar *p, int taps, double *out);
 int ltci_cuda_mgift(const double *cube, const ltci_radar *p, const double *ctilde, int n_ctilde,
                     int variant, double *out /* K*M complex */);
@@ -192,6 +213,10 @@ typedef struct {
 int ltci_cuda_extract_detections(const ltci_detection_map *map, const ltci_dual_space *space,
                                  const ltci_ambiguity *amb, double gamma, ltci_detection *out,
                                  int max_out, int *n_out);
+/* extract_detections for single-scale (FD-GRFT) maps: detection_from_cell
+ * proj/src/detection.cpp:101-111, cell sizes :59-63 */
+int ltci_cuda_extract_detections_single(const ltci_detection_map *map, const ltci_single_space *space,
+                                        double gamma, ltci_detection *out, int max_out, int *n_out);
 
 /* ---- engine: device-resident plan for streaming / benchmarking ---------- */
 typedef struct ltci_engine ltci_engine;

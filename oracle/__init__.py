@@ -20,7 +20,7 @@ import numpy as np
 
 from paper_2403_06788_b200 import _cabi as A
 from paper_2403_06788_b200.model import (AmbiguitySpace, DetectionMap, DetectorOptions, DualScaleSpace,  # noqa: F401
-                                         RadarParams, map_from_c)
+                                         RadarParams, SingleScaleSpace, map_from_c)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_PATH = os.path.join(HERE, "liboracle.so")
@@ -95,6 +95,11 @@ def ref():
                                        vp, P(C.c_int)]
         lib.ref_resolve_threads.argtypes = [C.c_int]
         lib.ref_write_cube_file.argtypes = [C.c_char_p, P(A.CCubeHeader), vp]
+        lib.ref_build_single_scale.argtypes = [P(A.CRadar), C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
+                                               C.c_int, C.c_int, P(A.CSingleSpace)]
+        lib.ref_fd_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
+        lib.ref_extract_single.argtypes = [P(A.CDetectionMap), P(A.CSingleSpace), C.c_double, C.c_int, vp,
+                                           P(C.c_int)]
         lib.ref_read_cube_file.argtypes = [C.c_char_p, P(A.CCubeHeader), vp, C.c_uint64]
         _ref = lib
     return _ref
@@ -302,3 +307,38 @@ def ref_read_cube_file(path, max_samples=1 << 24):
     _check(lib.ref_read_cube_file(str(path).encode(), C.byref(h), _vp(out), 2 * out.size), lib)
     p = RadarParams.from_c(h.radar)
     return int(h.domain), p, float(h.sigma2), out[: p.K * p.M].reshape(p.M, p.K).copy()
+
+
+# ----------------------------------------------- fd_grft (reference, C++) ---
+def ref_single_scale(params, P, bounds, alpha, roi_first, roi_last) -> SingleScaleSpace:
+    lib = ref()
+    lo = (C.c_double * P)(*[b[0] for b in bounds])
+    hi = (C.c_double * P)(*[b[1] for b in bounds])
+    al = (C.c_double * P)(*alpha)
+    r, s = params.to_c(), A.CSingleSpace()
+    _check(lib.ref_build_single_scale(C.byref(r), P, lo, hi, al, roi_first, roi_last, C.byref(s)), lib)
+    return SingleScaleSpace.from_c(s)
+
+
+def ref_fd(cube, params, space: SingleScaleSpace, opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    lib = ref()
+    opt = opt or DetectorOptions()
+    data = _c128(cube)
+    r, s, o = params.to_c(), space.to_c(), opt.to_c()
+    pm = A.PMap()
+    _check(lib.ref_fd_grft(_vp(data), C.byref(r), C.byref(s), C.byref(o), C.byref(pm)), lib)
+    m = _map(lib, pm, params, lib.ref_free_map)
+    m.single = space
+    return m
+
+
+def ref_extract_single(m: DetectionMap, gamma: float, max_out: int = 4096) -> np.ndarray:
+    """(statistic, c0..c3, flat) rows of the reference's extract_detections on an FD map."""
+    from paper_2403_06788_b200.detection import _to_c
+    lib = ref()
+    cm, keep = _to_c(m)
+    s = m.single.to_c()
+    rows = np.zeros((max_out, 6))
+    n = C.c_int(0)
+    _check(lib.ref_extract_single(C.byref(cm), C.byref(s), gamma, max_out, _vp(rows), C.byref(n)), lib)
+    return rows[: n.value]

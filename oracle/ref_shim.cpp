@@ -108,6 +108,34 @@ R::DualScaleSpace space_of(const ltci_dual_space& s) {
     return d;
 }
 
+R::SingleScaleSpace single_of(const ltci_single_space& s) {
+    R::SingleScaleSpace d;
+    d.params = radar_of(s.radar);
+    for (int p = 0; p < s.order; ++p) {
+        d.c.push_back(grid_of(s.c[p]));
+        d.steps.rm.push_back(s.rm_step[p]);
+        d.steps.dfm.push_back(s.dfm_step[p]);
+        d.steps.alpha.push_back(s.alpha[p]);
+    }
+    d.roi.first = s.roi_first;
+    d.roi.last = s.roi_last;
+    return d;
+}
+
+void single_to(const R::SingleScaleSpace& d, ltci_single_space* s) {
+    std::memset(s, 0, sizeof(*s));
+    radar_to(d.params, &s->radar);
+    s->order = d.order();
+    for (int p = 0; p < d.order() && p < LTCI_MAX_ORDER; ++p) {
+        s->c[p] = grid_to(d.c[p]);
+        s->rm_step[p] = d.steps.rm[p];
+        s->dfm_step[p] = d.steps.dfm[p];
+        s->alpha[p] = d.steps.alpha[p];
+    }
+    s->roi_first = d.roi.first;
+    s->roi_last = d.roi.last;
+}
+
 void space_to(const R::DualScaleSpace& d, ltci_dual_space* s) {
     std::memset(s, 0, sizeof(*s));
     radar_to(d.params, &s->radar);
@@ -500,6 +528,54 @@ int ref_read_cube_file(const char* path, ltci_cube_header* h, double* out, uint6
         h->sigma2 = f.sigma2;
         if (cap < 2 * f.data.size()) throw std::invalid_argument("ref_read_cube_file: buffer too small");
         copy_out(f.data, out);
+    });
+}
+
+// build_single_scale (proj/src/search_space.cpp:69-79)
+int ref_build_single_scale(const ltci_radar* r, int P, const double* lo, const double* hi, const double* alpha,
+                           int roi_first, int roi_last, ltci_single_space* out) {
+    return guarded([&] {
+        std::vector<R::Bounds> b(P);
+        for (int p = 0; p < P; ++p) b[p] = R::Bounds{lo[p], hi[p]};
+        std::vector<double> al(alpha, alpha + P);
+        single_to(R::build_single_scale(radar_of(*r), P, b, al, R::RangeRoi{roi_first, roi_last}), out);
+    });
+}
+
+// fd_grft (proj/src/detectors.cpp:105-197)
+int ref_fd_grft(const double* cube, const ltci_radar* r, const ltci_single_space* s, const ltci_options* o,
+                ltci_detection_map** out) {
+    return guarded([&] {
+        R::FreqPulseCube c = cube_of(cube, radar_of(*r));
+        *out = map_to(R::fd_grft(c, single_of(*s), options_of(o)));
+    });
+}
+
+// extract_detections (proj/src/detection.cpp:158-244) on a single-scale map
+int ref_extract_single(const ltci_detection_map* m, const ltci_single_space* s, double gamma, int max_out,
+                       double* rows, int* n_out) {
+    return guarded([&] {
+        R::DetectionMap map;
+        map.kind = static_cast<R::DetectorKind>(m->kind);
+        map.params = radar_of(s->radar);
+        for (int i = 0; i < m->n_axes; ++i)
+            map.axes.push_back(R::AxisDesc{static_cast<R::AxisDesc::Role>(m->axes[i].role),
+                                           m->axes[i].order, m->axes[i].size});
+        map.retain_threshold = m->retain_threshold;
+        map.single = single_of(*s);
+        for (std::uint64_t i = 0; i < m->n_candidates; ++i)
+            map.candidates.emplace_back(m->cand_index[i],
+                                        R::cplx(m->cand_value[2 * i], m->cand_value[2 * i + 1]));
+        std::vector<R::Detection> dets = R::extract_detections(map, gamma);
+        int n = std::min<int>(max_out, static_cast<int>(dets.size()));
+        for (int i = 0; i < n; ++i) {
+            double* row = rows + 6 * i;
+            row[0] = dets[i].statistic;
+            for (int k = 0; k < 4; ++k)
+                row[1 + k] = k < static_cast<int>(dets[i].estimate.c.size()) ? dets[i].estimate.c[k] : 0.0;
+            row[5] = static_cast<double>(map.encode(dets[i].cell));
+        }
+        *n_out = static_cast<int>(dets.size());
     });
 }
 

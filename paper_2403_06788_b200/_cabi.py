@@ -34,6 +34,12 @@ class CDualSpace(C.Structure):
                 ("roi_first", C.c_int32), ("roi_last", C.c_int32)]
 
 
+class CSingleSpace(C.Structure):
+    _fields_ = [("radar", CRadar), ("order", C.c_int32), ("c", CGrid * MAX_ORDER),
+                ("rm_step", C.c_double * MAX_ORDER), ("dfm_step", C.c_double * MAX_ORDER),
+                ("alpha", C.c_double * MAX_ORDER), ("roi_first", C.c_int32), ("roi_last", C.c_int32)]
+
+
 class CAmbiguity(C.Structure):
     _fields_ = [("q_min", C.c_int32), ("q_max", C.c_int32)]
 

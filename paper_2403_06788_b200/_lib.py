@@ -21,7 +21,7 @@ EXPORTS = (
     "ltci_cuda_mgift", "ltci_cuda_gft", "ltci_cuda_detection_threshold", "ltci_engine_create",
     "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
     "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path",
-    "ltci_engine_work", "ltci_engine_run_file",
+    "ltci_engine_work", "ltci_engine_run_file", "ltci_cuda_fd_grft", "ltci_cuda_extract_detections_single",
     "ltci_cuda_extract_detections", "ltci_cuda_cube_file_info", "ltci_cuda_cube_file_read",
     "ltci_cuda_cube_file_write", "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
 )
@@ -95,6 +95,9 @@ def load():
     lib.ltci_cuda_cube_file_read.argtypes = [C.c_char_p, P(A.CCubeHeader), vp, C.c_uint64]
     lib.ltci_cuda_cube_file_write.argtypes = [C.c_char_p, P(A.CCubeHeader), vp]
     lib.ltci_engine_run_file.argtypes = [vp, C.c_char_p, vp]
+    lib.ltci_cuda_fd_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
+    lib.ltci_cuda_extract_detections_single.argtypes = [P(A.CDetectionMap), P(A.CSingleSpace), C.c_double,
+                                                        P(A.CDetection), C.c_int, P(C.c_int)]
     lib.ltci_cuda_last_error.restype = C.c_char_p
     lib.ltci_cuda_version.restype = C.c_int
     _lib = lib

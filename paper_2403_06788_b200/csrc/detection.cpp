@@ -27,7 +27,8 @@ constexpr double kC = 3.0e8;
 
 struct Ctx {
     const ltci_detection_map* map;
-    const ltci_dual_space* s;
+    const ltci_dual_space* s;      // DS maps
+    const ltci_single_space* ss;   // FD maps
     const ltci_ambiguity* amb;
     int M;
     double dR, va;
@@ -58,11 +59,22 @@ double grid_value(const ltci_grid& g, int i) { return g.start + g.step * static_
 
 ltci_detection from_cell(const Ctx& x, const std::vector<int>& cell, double re, double im, uint64_t idx) {
     const ltci_detection_map& m = *x.map;
-    const ltci_dual_space& s = *x.s;
     ltci_detection d;
     std::memset(&d, 0, sizeof(d));
     d.statistic = std::hypot(re, im);
     d.flat_index = idx;
+    if (m.kind == LTCI_FD_GRFT) {
+        // detection.cpp:101-111: c0 = n dR, c_p = grid value of the order-p axis
+        const ltci_single_space& ss = *x.ss;
+        const int n = cell[axis_index(m, LTCI_AXIS_RANGE)] + ss.roi_first;
+        d.n_coef = ss.order + 1;
+        d.c[0] = n * x.dR;
+        for (int ord = 1; ord <= ss.order; ++ord)
+            d.c[ord] = grid_value(ss.c[ord - 1],
+                                  cell[axis_index(m, ord == 1 ? LTCI_AXIS_VELOCITY : LTCI_AXIS_HIGHER, ord)]);
+        return d;
+    }
+    const ltci_dual_space& s = *x.s;
     const int n = cell[axis_index(m, LTCI_AXIS_RANGE)] + s.roi_first;
     const int jd = cell[axis_index(m, LTCI_AXIS_DOPPLER)];
     if (m.kind == LTCI_DS_GRFT) {
@@ -93,19 +105,14 @@ ltci_detection from_cell(const Ctx& x, const std::vector<int>& cell, double re, 
 
 void ltcib_set_last_error(const char* msg);  // engine.cu: backs ltci_cuda_last_error()
 
-extern "C" int ltci_cuda_extract_detections(const ltci_detection_map* map, const ltci_dual_space* space,
-                                            const ltci_ambiguity* amb, double gamma, ltci_detection* out,
-                                            int max_out, int* n_out) {
+namespace {
+
+int extract_impl(const Ctx& x, double gamma, ltci_detection* out, int max_out, int* n_out, double cs_vel) {
+    const ltci_detection_map* map = x.map;
     try {
-        if (!map || !space || !n_out) throw std::invalid_argument("extract_detections: null argument");
-        if (map->kind != LTCI_DS_GRFT && map->kind != LTCI_DS_KT_MFP)
-            throw std::invalid_argument("extract_detections: only dual-scale maps are produced here");
-        if (map->kind == LTCI_DS_KT_MFP && !amb) throw std::invalid_argument("extract_detections: ambiguity needed");
         if (gamma < 0) throw std::invalid_argument("extract_detections: gamma must be >= 0");
         if (gamma < map->retain_threshold)
             throw std::invalid_argument("extract_detections: gamma below the map's retention threshold");
-        Ctx x{map, space, amb, space->radar.M, kC / (2.0 * space->radar.fs),
-              (kC / space->radar.fc) * space->radar.PRF / 2.0};
 
         // Local-max test only needs neighbours above gamma: anything dropped by
         // retention is below the candidate under test (detection.cpp:165-168).
@@ -158,7 +165,6 @@ extern "C" int ltci_cuda_extract_detections(const ltci_detection_map* map, const
 
         // cluster merge along the range/velocity ridge (detection.cpp:209-243)
         const double cs_range = x.dR;
-        const double cs_vel = map->kind == LTCI_DS_GRFT ? (x.va / x.M) / space->kappa : x.va / x.M;
         std::sort(raw.begin(), raw.end(), [](const ltci_detection& a, const ltci_detection& b) {
             if (a.statistic != b.statistic) return a.statistic > b.statistic;
             return a.flat_index < b.flat_index;
@@ -196,4 +202,43 @@ extern "C" int ltci_cuda_extract_detections(const ltci_detection_map* map, const
         ltcib_set_last_error(e.what());
         return LTCI_RUNTIME_ERROR;
     }
+}
+
+}  // namespace
+
+extern "C" int ltci_cuda_extract_detections(const ltci_detection_map* map, const ltci_dual_space* space,
+                                            const ltci_ambiguity* amb, double gamma, ltci_detection* out,
+                                            int max_out, int* n_out) {
+    if (!map || !space || !n_out) {
+        ltcib_set_last_error("extract_detections: null argument");
+        return LTCI_INVALID_ARGUMENT;
+    }
+    if (map->kind != LTCI_DS_GRFT && map->kind != LTCI_DS_KT_MFP) {
+        ltcib_set_last_error("extract_detections: dual-scale map expected (use _single for FD-GRFT)");
+        return LTCI_INVALID_ARGUMENT;
+    }
+    if (map->kind == LTCI_DS_KT_MFP && !amb) {
+        ltcib_set_last_error("extract_detections: ambiguity needed");
+        return LTCI_INVALID_ARGUMENT;
+    }
+    const double va = (kC / space->radar.fc) * space->radar.PRF / 2.0;
+    Ctx x{map, space, nullptr, amb, space->radar.M, kC / (2.0 * space->radar.fs), va};
+    // estimate_cell_sizes (detection.cpp:55-79)
+    const double cs_vel = map->kind == LTCI_DS_GRFT ? (va / x.M) / space->kappa : va / x.M;
+    return extract_impl(x, gamma, out, max_out, n_out, cs_vel);
+}
+
+extern "C" int ltci_cuda_extract_detections_single(const ltci_detection_map* map, const ltci_single_space* space,
+                                                   double gamma, ltci_detection* out, int max_out, int* n_out) {
+    if (!map || !space || !n_out) {
+        ltcib_set_last_error("extract_detections: null argument");
+        return LTCI_INVALID_ARGUMENT;
+    }
+    if (map->kind != LTCI_FD_GRFT) {
+        ltcib_set_last_error("extract_detections_single: FD-GRFT map expected");
+        return LTCI_INVALID_ARGUMENT;
+    }
+    const double va = (kC / space->radar.fc) * space->radar.PRF / 2.0;
+    Ctx x{map, nullptr, space, nullptr, space->radar.M, kC / (2.0 * space->radar.fs), va};
+    return extract_impl(x, gamma, out, max_out, n_out, space->c[0].step);  // detection.cpp:59-63
 }

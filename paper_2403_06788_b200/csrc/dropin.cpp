@@ -1,4 +1,4 @@
-// dropin.cpp -- ltci::ds_grft / ltci::ds_kt_mfp on the B200 (libltci_b200.so).
+// dropin.cpp -- ltci::ds_grft / ltci::ds_kt_mfp / ltci::fd_grft on the B200 (libltci_b200.so).
 //
 // Same signatures, argument meaning and exceptions as the reference
 // (proj/include/ltci/detectors.hpp:42-48, proj/src/detectors.cpp:414-481):
@@ -45,6 +45,23 @@ ltci_dual_space to_c(const ltci::DualScaleSpace& s) {
     }
     if (s.steps.rm.empty()) throw std::invalid_argument("ds detector: space has no step sizes");
     d.kappa = s.kappa;
+    d.roi_first = s.roi.first;
+    d.roi_last = s.roi.last;
+    return d;
+}
+
+ltci_single_space to_c(const ltci::SingleScaleSpace& s) {
+    ltci_single_space d;
+    std::memset(&d, 0, sizeof(d));
+    d.radar = to_c(s.params);
+    if (s.c.empty() || s.c.size() > LTCI_MAX_ORDER) throw std::invalid_argument("fd_grft: space order must be 1..4");
+    d.order = static_cast<int32_t>(s.c.size());
+    for (int p = 0; p < d.order; ++p) {
+        d.c[p] = ltci_grid{s.c[p].start, s.c[p].step, s.c[p].count};
+        d.rm_step[p] = p < static_cast<int>(s.steps.rm.size()) ? s.steps.rm[p] : 0.0;
+        d.dfm_step[p] = p < static_cast<int>(s.steps.dfm.size()) ? s.steps.dfm[p] : 0.0;
+        d.alpha[p] = p < static_cast<int>(s.steps.alpha.size()) ? s.steps.alpha[p] : 0.0;
+    }
     d.roi_first = s.roi.first;
     d.roi_last = s.roi.last;
     return d;
@@ -110,6 +127,21 @@ namespace ltci {
 
 DetectionMap ds_grft(const FreqPulseCube& cube, const DualScaleSpace& space, const DetectorOptions& opt) {
     return ltci_b200::ds_grft_with_peaks(cube, space, opt, nullptr);
+}
+
+// proj/src/detectors.cpp:105-197
+DetectionMap fd_grft(const FreqPulseCube& cube, const SingleScaleSpace& space, const DetectorOptions& opt) {
+    const ltci_radar r = to_c(cube.params);
+    const ltci_single_space s = to_c(space);
+    const ltci_options o = to_c(opt);
+    MapGuard g;
+    const std::size_t n = static_cast<std::size_t>(cube.params.K) * cube.params.M;
+    if (cube.data.size() != n) throw std::invalid_argument("detector: cube data size does not match K*M");
+    const int rc = ltci_cuda_fd_grft(reinterpret_cast<const double*>(cube.data.data()), &r, &s, &o, &g.m);
+    if (rc != LTCI_OK) rethrow(rc);
+    DetectionMap m = to_cpp(*g.m, cube.params);
+    m.single = space;
+    return m;
 }
 
 DetectionMap ds_kt_mfp(const FreqPulseCube& cube, const AmbiguitySpace& amb, const DualScaleSpace& space,

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -26,6 +27,7 @@
 #include "cube_io.hpp"
 #include "fine_fft.cuh"
 #include "fine_tc.cuh"
+#include "fd_grft.cuh"
 
 using namespace ltcib;
 
@@ -810,6 +812,41 @@ void* xmalloc(size_t bytes) {
     return p;
 }
 
+struct CandSortBufs {
+    DevBuf<unsigned long long>& k0;
+    DevBuf<unsigned long long>& k1;
+    DevBuf<float2>& v0;
+    DevBuf<float2>& v1;
+    DevBuf<double2>& out;
+    DevBuf<unsigned char>& tmp;
+};
+
+// Candidates: radix sort by flat index and recentre on the device (D = 1,
+// dop_first = M/2 is the identity), then one D2H per array straight into the
+// map (scales to 1e8+ retained cells).
+void sort_candidates(const CandRec* d_cand, unsigned long long count, unsigned long long cells, int D,
+                     int dop_first, int M, CandSortBufs& b, uint64_t* h_idx, double* h_val, cudaStream_t st) {
+    b.k0.ensure(count);
+    b.k1.ensure(count);
+    b.v0.ensure(count);
+    b.v1.ensure(count);
+    b.out.ensure(count);
+    const int blocks = static_cast<int>(std::min<unsigned long long>((count + 255) / 256, 148 * 8));
+    cand_split_kernel<<<blocks, 256, 0, st>>>(d_cand, b.k0.p, b.v0.p, count);
+    CK(cudaGetLastError());
+    int end_bit = 1;
+    while (end_bit < 64 && (cells >> end_bit) != 0) ++end_bit;
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, b.k0.p, b.k1.p, b.v0.p, b.v1.p, count, 0, end_bit, st));
+    b.tmp.ensure(tmp);
+    CK(cub::DeviceRadixSort::SortPairs(b.tmp.p, tmp, b.k0.p, b.k1.p, b.v0.p, b.v1.p, count, 0, end_bit, st));
+    cand_recenter_kernel<<<blocks, 256, 0, st>>>(b.k1.p, b.v1.p, b.out.p, count, D, dop_first, M);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h_idx, b.k1.p, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_val, b.out.p, count * sizeof(double2), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+}
+
 ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
     const Plan& pl = e->pl;
     DeviceGuard dg(e->device);
@@ -879,30 +916,11 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         out->cand_index = static_cast<uint64_t*>(xmalloc(count * sizeof(uint64_t)));
         out->cand_value = static_cast<double*>(xmalloc(2 * count * sizeof(double)));
         if (count) {
-            e->ck0.ensure(count);
-            e->ck1.ensure(count);
-            e->cv0.ensure(count);
-            e->cv1.ensure(count);
-            e->cvals.ensure(count);
-            const int blocks = static_cast<int>(std::min<unsigned long long>((count + 255) / 256, 148 * 8));
-            cand_split_kernel<<<blocks, 256, 0, st>>>(e->cand.p, e->ck0.p, e->cv0.p, count);
-            CK(cudaGetLastError());
             const unsigned long long cells = static_cast<unsigned long long>(pl.coarse_cells) * pl.fine_cells *
                                              static_cast<unsigned long long>(pl.R_total) * pl.D;
-            int end_bit = 1;
-            while (end_bit < 64 && (cells >> end_bit) != 0) ++end_bit;
-            size_t tmp = 0;
-            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, e->ck0.p, e->ck1.p, e->cv0.p, e->cv1.p, count, 0,
-                                               end_bit, st));
-            e->csort_tmp.ensure(tmp);
-            CK(cub::DeviceRadixSort::SortPairs(e->csort_tmp.p, tmp, e->ck0.p, e->ck1.p, e->cv0.p, e->cv1.p, count,
-                                               0, end_bit, st));
-            cand_recenter_kernel<<<blocks, 256, 0, st>>>(e->ck1.p, e->cv1.p, e->cvals.p, count, pl.D, pl.dop_first,
-                                                         pl.rp.M);
-            CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(out->cand_index, e->ck1.p, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(out->cand_value, e->cvals.p, count * sizeof(double2), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            CandSortBufs b{e->ck0, e->ck1, e->cv0, e->cv1, e->cvals, e->csort_tmp};
+            sort_candidates(e->cand.p, count, cells, pl.D, pl.dop_first, pl.rp.M, b, out->cand_index,
+                            out->cand_value, st);
         }
         if (pl.keep_dense) {
             out->dense_stored = 1;
@@ -956,6 +974,208 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, f
 
 }  // namespace
 
+namespace {
+
+// ---- fd_grft (reference proj/src/detectors.cpp:105-197)
+template <int K>
+void fd_launch_batch(const FdArgs& a, cudaStream_t st) {
+    auto mf = fd_mf_kernel<K>;
+    const size_t smem_mf = 2ull * kFdCells * a.M * sizeof(unsigned);
+    auto sc = fd_fft_scan_kernel<K>;
+    constexpr int PG = kCoarseSamples / K;
+    const size_t smem_sc = static_cast<size_t>(PG) * coarse_kp(K) * sizeof(float2);
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(mf, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        CK(cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_done = true;
+    }
+    mf<<<static_cast<unsigned>((a.c_count + kFdCells - 1) / kFdCells), kFdThreads, smem_mf, st>>>(a);
+    CK(cudaGetLastError());
+    sc<<<static_cast<unsigned>((a.c_count + PG - 1) / PG), kCoarseThreads, smem_sc, st>>>(a);
+    CK(cudaGetLastError());
+}
+
+void fd_launch(const FdArgs& a, cudaStream_t st) {
+    switch (a.K) {
+        case 16: fd_launch_batch<16>(a, st); break;
+        case 32: fd_launch_batch<32>(a, st); break;
+        case 64: fd_launch_batch<64>(a, st); break;
+        case 128: fd_launch_batch<128>(a, st); break;
+        case 256: fd_launch_batch<256>(a, st); break;
+        case 512: fd_launch_batch<512>(a, st); break;
+        case 1024: fd_launch_batch<1024>(a, st); break;
+        case 2048: fd_launch_batch<2048>(a, st); break;
+        case 4096: fd_launch_batch<4096>(a, st); break;
+        case 8192: fd_launch_batch<8192>(a, st); break;
+        default: fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: unsupported K");
+    }
+}
+
+ltci_detection_map* fd_grft_run(const double* cube, const ltci_radar& rp, const ltci_single_space& s,
+                                const ltci_options* opt) {
+    validate_radar(rp);
+    check_same_params(rp, s.radar);
+    if (rp.K < 16 || rp.K > 8192) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be in [16, 8192]");
+    if (rp.M > 4096) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: fd_grft supports M <= 4096");
+    const int P = s.order;
+    if (P < 1 || P > LTCI_MAX_ORDER) fail(LTCI_INVALID_ARGUMENT, "fd_grft: order must be in [1, 4]");
+    unsigned long long cells = 1;
+    for (int p = 0; p < P; ++p) {
+        if (s.c[p].count < 1) fail(LTCI_INVALID_ARGUMENT, "grid is empty");
+        cells *= static_cast<unsigned long long>(s.c[p].count);
+    }
+    if (s.roi_first < 0 || s.roi_last >= rp.K || s.roi_first > s.roi_last)
+        fail(LTCI_INVALID_ARGUMENT, "fd_grft: ROI outside the range axis");
+    const int R = s.roi_last - s.roi_first + 1;
+    const int device = opt ? opt->device : 0;
+    const double retain = opt ? opt->retain_threshold : 0.0;
+    const bool keep_dense = opt && opt->keep_dense;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
+    if (device < 0 || device >= ndev) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad device ordinal");
+    DeviceGuard dg(device);
+    cudaStream_t st = nullptr;
+    const int K = rp.K, M = rp.M;
+    const size_t n = static_cast<size_t>(K) * M;
+    // per-thread, per-device workspace: grow-only buffers reused across calls
+    // (many small calls -- e.g. noise-only Monte-Carlo trials -- pay no cudaMalloc)
+    struct FdWorkspace {
+        DevBuf<double2> f64;
+        DevBuf<float2> c64, acc, dense;
+        DevBuf<CandRec> cand;
+        DevBuf<unsigned long long> ccount, k0, k1;
+        DevBuf<PeakSlot> best;
+        DevBuf<float2> v0, v1;
+        DevBuf<double2> vo;
+        DevBuf<unsigned char> tmp;
+    };
+    thread_local std::vector<std::unique_ptr<FdWorkspace>> pool;
+    if (static_cast<int>(pool.size()) <= device) pool.resize(device + 1);
+    if (!pool[device]) pool[device] = std::make_unique<FdWorkspace>();
+    FdWorkspace& w = *pool[device];
+    auto& f64 = w.f64;
+    auto& c64 = w.c64;
+    auto& acc = w.acc;
+    auto& dense = w.dense;
+    auto& cand = w.cand;
+    auto& ccount = w.ccount;
+    auto& best = w.best;
+    f64.ensure(n);
+    c64.ensure(n);
+    CK(cudaMemcpyAsync(f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice, st));
+    f64_to_c64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(f64.p, c64.p, n);
+    CK(cudaGetLastError());
+
+    size_t free_b = 0, total_b = 0;
+    if (keep_dense) {
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const double bytes = static_cast<double>(cells) * R * sizeof(float2);
+        if (bytes > 0.5 * static_cast<double>(free_b) || bytes * 2 > 64.0 * (1ull << 30))
+            fail(LTCI_BAD_ALLOC, "ltci_cuda: dense fd_grft map exceeds the result memory");
+        dense.ensure(static_cast<size_t>(cells) * R);
+    }
+    // MF output per batch: bounded at 2 GiB, whole CTAs of both kernels
+    const unsigned long long gran = std::max<unsigned long long>(kFdCells, kCoarseSamples / K);
+    unsigned long long batch = std::max<unsigned long long>(gran, ((2ull << 30) / (8ull * K)) / gran * gran);
+    batch = std::min(batch, (cells + gran - 1) / gran * gran);
+    acc.ensure(static_cast<size_t>(batch) * K);
+    ccount.ensure(1);
+    best.ensure(1);
+
+    FdArgs a{};
+    a.cube = c64.p;
+    a.acc = acc.p;
+    a.K = K;
+    a.M = M;
+    a.P = P;
+    for (int p = 0; p < P; ++p) {
+        a.count[p] = s.c[p].count;
+        a.start[p] = s.c[p].start;
+        a.step[p] = s.c[p].step;
+    }
+    a.inv_prf = 1.0 / rp.PRF;
+    a.two_over_lambda = 2.0 / lambda_of(rp);
+    a.two_df_over_c = 2.0 * rp.delta_f / kC;
+    a.roi_first = s.roi_first;
+    a.R = R;
+    a.retain2 = retain < 0 ? -1.0f : static_cast<float>(retain * retain);
+    a.dense = keep_dense ? dense.p : nullptr;
+    a.best = best.p;
+    a.cand_count = ccount.p;
+
+    unsigned long long cap = std::max<unsigned long long>(cand.n, 1ull << 16), count = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        cand.ensure(cap);
+        a.cand = cand.p;
+        a.cand_cap = cap;
+        CK(cudaMemsetAsync(ccount.p, 0, sizeof(unsigned long long), st));
+        const PeakSlot init{0.f, 0.f, ~0ull};
+        CK(cudaMemcpyAsync(best.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+        for (unsigned long long c0 = 0; c0 < cells; c0 += batch) {
+            a.c_begin = c0;
+            a.c_count = std::min(batch, cells - c0);
+            fd_launch(a, st);
+        }
+        CK(cudaMemcpyAsync(&count, ccount.p, sizeof(count), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (count <= cap) break;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        if (static_cast<double>(count) * 64.0 > 0.8 * static_cast<double>(free_b) ||
+            static_cast<double>(count) * 24.0 > 64.0 * (1ull << 30))
+            fail(LTCI_BAD_ALLOC, "ltci_cuda: " + std::to_string(count) +
+                                     " retained cells exceed the result memory (raise retain_threshold)");
+        cap = count;
+    }
+
+    auto* out = static_cast<ltci_detection_map*>(std::calloc(1, sizeof(ltci_detection_map)));
+    if (!out) throw std::bad_alloc();
+    try {
+        out->kind = LTCI_FD_GRFT;
+        // single_scale_axes (detectors.cpp:94-101): c_P .. c_2, c_1, range
+        int na = 0;
+        for (int p = P; p >= 2; --p) out->axes[na++] = ltci_axis{LTCI_AXIS_HIGHER, p, s.c[p - 1].count};
+        out->axes[na++] = ltci_axis{LTCI_AXIS_VELOCITY, 1, s.c[0].count};
+        out->axes[na++] = ltci_axis{LTCI_AXIS_RANGE, 0, R};
+        out->n_axes = na;
+        out->counters[1] = cells * static_cast<unsigned long long>(K);  // mf += n0() per cell
+        out->counters[2] = cells;                                       // ifft += 1 per cell
+        out->retain_threshold = retain;
+        PeakSlot b{};
+        CK(cudaMemcpy(&b, best.p, sizeof(b), cudaMemcpyDeviceToHost));
+        out->argmax = b.idx;
+        out->argmax_value[0] = b.re;
+        out->argmax_value[1] = b.im;
+        out->n_candidates = count;
+        out->cand_index = static_cast<uint64_t*>(xmalloc(count * sizeof(uint64_t)));
+        out->cand_value = static_cast<double*>(xmalloc(2 * count * sizeof(double)));
+        if (count) {
+            CandSortBufs bufs{w.k0, w.k1, w.v0, w.v1, w.vo, w.tmp};
+            sort_candidates(cand.p, count, cells * static_cast<unsigned long long>(R), 1, M / 2, M, bufs,
+                            out->cand_index, out->cand_value, st);
+        }
+        if (keep_dense) {
+            const size_t nd = static_cast<size_t>(cells) * R;
+            std::vector<float2> h(nd);
+            CK(cudaMemcpy(h.data(), dense.p, nd * sizeof(float2), cudaMemcpyDeviceToHost));
+            out->dense_stored = 1;
+            out->dense_count = nd;
+            out->dense = static_cast<double*>(xmalloc(2 * nd * sizeof(double)));
+            for (size_t i = 0; i < nd; ++i) {
+                out->dense[2 * i] = h[i].x;
+                out->dense[2 * i + 1] = h[i].y;
+            }
+        }
+    } catch (...) {
+        ltci_cuda_free_map(out);
+        throw;
+    }
+    return out;
+}
+
+}  // namespace
+
 extern "C" {
 
 int ltci_cuda_measure_fp32_peak(int device, double* tflops) {
@@ -996,6 +1216,14 @@ void ltci_cuda_free_map(ltci_detection_map* m) {
     std::free(m->peak_index);
     std::free(m->peak_value);
     std::free(m);
+}
+
+int ltci_cuda_fd_grft(const double* cube, const ltci_radar* cube_params, const ltci_single_space* space,
+                      const ltci_options* opt, ltci_detection_map** out) {
+    return guarded([&] {
+        if (!cube || !cube_params || !space || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        *out = fd_grft_run(cube, *cube_params, *space, opt);
+    });
 }
 
 int ltci_cuda_ds_grft(const double* cube, const ltci_radar* cube_params, const ltci_dual_space* space,

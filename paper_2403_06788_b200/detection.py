@@ -48,18 +48,25 @@ def _to_c(m: DetectionMap):
 def extract_detections(m: DetectionMap, gamma: float) -> List[Detection]:
     lib = _lib.load()
     cm, keep = _to_c(m)
-    s = m.dual.to_c()
-    a = m.amb.to_c() if m.amb is not None else None
     cap = max(16, min(int(m.cand_index.size), 1 << 20))
-    out = (A.CDetection * cap)()
     n = C.c_int(0)
-    _lib.raise_for(lib.ltci_cuda_extract_detections(C.byref(cm), C.byref(s), C.byref(a) if a is not None else None,
-                                                    gamma, out, cap, C.byref(n)), lib)
+    if m.kind == A.FD_GRFT:
+        ss = m.single.to_c()
+
+        def call(buf, k):
+            return lib.ltci_cuda_extract_detections_single(C.byref(cm), C.byref(ss), gamma, buf, k, C.byref(n))
+    else:
+        s = m.dual.to_c()
+        a = m.amb.to_c() if m.amb is not None else None
+
+        def call(buf, k):
+            return lib.ltci_cuda_extract_detections(C.byref(cm), C.byref(s), C.byref(a) if a is not None else None,
+                                                    gamma, buf, k, C.byref(n))
+    out = (A.CDetection * cap)()
+    _lib.raise_for(call(out, cap), lib)
     if n.value > cap:
         out = (A.CDetection * n.value)()
-        _lib.raise_for(lib.ltci_cuda_extract_detections(C.byref(cm), C.byref(s),
-                                                        C.byref(a) if a is not None else None, gamma, out,
-                                                        n.value, C.byref(n)), lib)
+        _lib.raise_for(call(out, n.value), lib)
     del keep
     res = []
     for i in range(n.value):

@@ -20,8 +20,8 @@ import numpy as np
 
 from . import _cabi as A
 from . import _lib
-from .model import (AmbiguitySpace, DetectionMap, DetectorOptions, DualScaleSpace, RadarParams, cube_as_f64,
-                    map_from_c)
+from .model import (AmbiguitySpace, DetectionMap, DetectorOptions, DualScaleSpace, RadarParams, SingleScaleSpace,
+                    cube_as_f64, map_from_c)
 
 
 def _f64_ptr(a: np.ndarray):
@@ -61,6 +61,21 @@ def ds_kt_mfp(cube: np.ndarray, params: RadarParams, amb: AmbiguitySpace, space:
                                            C.byref(pm)), lib)
     m = _take_map(lib, pm, params)
     m.dual, m.amb = space, amb
+    return m
+
+
+def fd_grft(cube: np.ndarray, params: RadarParams, space: SingleScaleSpace,
+            opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    """Single-scale frequency-domain GRFT on the GPU (ltci::fd_grft,
+    proj/src/detectors.cpp:105-197)."""
+    lib = _lib.load()
+    opt = opt or DetectorOptions()
+    data = cube_as_f64(cube, params)
+    r, s, o = params.to_c(), space.to_c(), opt.to_c()
+    pm = A.PMap()
+    _lib.raise_for(lib.ltci_cuda_fd_grft(_f64_ptr(data), C.byref(r), C.byref(s), C.byref(o), C.byref(pm)), lib)
+    m = _take_map(lib, pm, params)
+    m.single = space
     return m
 
 

@@ -259,6 +259,60 @@ def build_dual_scale(params: RadarParams, P: int, bounds: Sequence[Bounds], alph
 
 
 @dataclass
+class SingleScaleSpace:
+    """SingleScaleSpace (proj/include/ltci/search_space.hpp:50-58)."""
+    params: RadarParams = field(default_factory=RadarParams)
+    steps: StepSizes = field(default_factory=StepSizes)
+    c: List[Grid] = field(default_factory=list)
+    roi: RangeRoi = field(default_factory=RangeRoi)
+
+    def order(self) -> int:
+        return len(self.c)
+
+    def cells(self) -> int:
+        n = 1
+        for g in self.c:
+            n *= g.count
+        return n
+
+    def to_c(self) -> A.CSingleSpace:
+        c = A.CSingleSpace()
+        c.radar = self.params.to_c()
+        c.order = self.order()
+        if not 1 <= c.order <= A.MAX_ORDER:
+            raise ValueError("single-scale space: order must be in 1..4")
+        for p in range(c.order):
+            g = self.c[p]
+            c.c[p] = A.CGrid(g.start, g.step, g.count)
+            c.rm_step[p] = self.steps.rm[p] if p < len(self.steps.rm) else 0.0
+            c.dfm_step[p] = self.steps.dfm[p] if p < len(self.steps.dfm) else 0.0
+            c.alpha[p] = self.steps.alpha[p] if p < len(self.steps.alpha) else 0.0
+        c.roi_first, c.roi_last = self.roi.first, self.roi.last
+        return c
+
+    @staticmethod
+    def from_c(c: A.CSingleSpace) -> "SingleScaleSpace":
+        s = SingleScaleSpace(params=RadarParams.from_c(c.radar), roi=RangeRoi(c.roi_first, c.roi_last))
+        for p in range(c.order):
+            s.c.append(Grid(c.c[p].start, c.c[p].step, c.c[p].count))
+            s.steps.rm.append(c.rm_step[p])
+            s.steps.dfm.append(c.dfm_step[p])
+            s.steps.alpha.append(c.alpha[p])
+        return s
+
+
+def build_single_scale(params: RadarParams, P: int, bounds: Sequence[Bounds], alpha: Sequence[float],
+                       roi: RangeRoi) -> SingleScaleSpace:
+    """build_single_scale (proj/src/search_space.cpp:69-79): every order at its DFM step."""
+    if len(bounds) != P:
+        raise ValueError("build_single_scale: bounds must have P entries")
+    s = SingleScaleSpace(params=params, steps=step_sizes(params, P, alpha), roi=roi)
+    for p in range(P):
+        s.c.append(span_grid(bounds[p], s.steps.dfm[p], False))
+    return s
+
+
+@dataclass
 class AmbiguitySpace:
     q_min: int = 0
     q_max: int = 0
@@ -331,6 +385,7 @@ class DetectionMap:
     argmax_value: complex = 0j
     dual: Optional[DualScaleSpace] = None
     amb: Optional[AmbiguitySpace] = None
+    single: Optional[SingleScaleSpace] = None
     doppler_first: int = 0
     peak_index: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
     peak_value: np.ndarray = field(default_factory=lambda: np.zeros(0, np.complex128))

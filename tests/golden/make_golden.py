@@ -17,6 +17,11 @@ what the reference's own functions return:
                    candidates, argmax, counters -- and the per-range-cell peak
                    map from ref_peak_map (reference mgift+gft in run_dual_scale's loop)
   p1_p3.npz        order-1 and order-3 ds_grft (dense) on a tiny instance
+  fd.npz           fd_grft at orders 1, 2 and 3 on
+                   build_single_scale spaces, keep_dense + candidates; the order-2
+                   case with a sub-ROI
+
+    python tests/golden/make_golden.py [fd]     (fd: only fd.npz)
 """
 from __future__ import annotations
 
@@ -60,8 +65,36 @@ def map_arrays(prefix, m):
             **({prefix + "dense": m.dense} if m.dense_stored else {})}
 
 
+def single_arrays(prefix, s):
+    return {prefix + "c": np.array([[g.start, g.step, g.count] for g in s.c]),
+            prefix + "steps": np.array([s.steps.rm, s.steps.dfm, s.steps.alpha]),
+            prefix + "roi": np.array([s.roi.first, s.roi.last])}
+
+
+def make_fd():
+    p = O.ref_radar(8 * 100e6, 100e6, 50e6, 2000.0, 32, 64)
+    tgt = [(0.4 + 0.1j, [21 * p.delta_R(), 13.3, 240.0]), (0.3, [40 * p.delta_R(), -22.0, -400.0])]
+    cube = c64(O.ref_synthesize(p, tgt, 1.0 / p.K, 91))
+    spaces = {"s2_": O.ref_single_scale(p, 2, [(-30.0, 30.0), (-1100.0, 1100.0)], [0.5, 0.5], 3, p.K - 5),
+              "s1_": O.ref_single_scale(p, 1, [(-30.0, 30.0)], [1.0], 0, p.K - 1),
+              "s3_": O.ref_single_scale(p, 3, [(-20.0, 20.0), (-450.0, 450.0), (-30000.0, 30000.0)],
+                                        [0.4, 0.3, 0.3], 0, p.K - 1)}
+    # retention at the 80th percentile of the order-2 dense map
+    probe = O.ref_fd(cube, p, spaces["s2_"], DetectorOptions(keep_dense=True))
+    retain = float(np.quantile(np.abs(probe.dense), 0.8))
+    opt = DetectorOptions(retain_threshold=retain, keep_dense=True)
+    out = {"cube": cube.astype(np.complex64), "retain": np.array(retain), **radar_arrays("", p)}
+    for key, sp in spaces.items():
+        out.update(single_arrays(key, sp), **map_arrays("m" + key[1:], O.ref_fd(cube, p, sp, opt)))
+    np.savez_compressed(os.path.join(HERE, "fd.npz"), **out)
+
+
 def main():
     assert O.have_ref(), "build the reference first: make -C oracle"
+    if sys.argv[1:] == ["fd"]:
+        make_fd()
+        print("fd.npz written to", HERE)
+        return
     # ---- transforms
     p = O.ref_radar(4 * 100e6, 100e6, 50e6, 2000.0, 32, 64)
     cube = c64(scene.add_noise(np.zeros((p.M, p.K), complex), 1.0, 101))
@@ -112,6 +145,7 @@ def main():
     pi, pv = O.ref_peak_map(cube, w.params, w.space)
     np.savez_compressed(os.path.join(HERE, "c0.npz"), cube=cube.astype(np.complex64), gamma=np.array(gamma),
                         peak_index=pi, peak_value=pv, **map_arrays("", m))
+    make_fd()
     print("golden vectors written to", HERE)
 
 
