@@ -980,17 +980,16 @@ namespace {
 template <int K>
 void fd_launch_batch(const FdArgs& a, cudaStream_t st) {
     auto mf = fd_mf_kernel<K>;
-    const size_t smem_mf = 2ull * kFdCells * a.M * sizeof(unsigned);
+    const size_t smem_mf = 0;
     auto sc = fd_fft_scan_kernel<K>;
     constexpr int PG = kCoarseSamples / K;
     const size_t smem_sc = static_cast<size_t>(PG) * coarse_kp(K) * sizeof(float2);
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
-        CK(cudaFuncSetAttribute(mf, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         CK(cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_done = true;
     }
-    mf<<<static_cast<unsigned>((a.c_count + kFdCells - 1) / kFdCells), kFdThreads, smem_mf, st>>>(a);
+    mf<<<static_cast<unsigned>((a.c_count + fd_cells(K) - 1) / fd_cells(K)), fd_threads(K), smem_mf, st>>>(a);
     CK(cudaGetLastError());
     sc<<<static_cast<unsigned>((a.c_count + PG - 1) / PG), kCoarseThreads, smem_sc, st>>>(a);
     CK(cudaGetLastError());
@@ -1017,7 +1016,7 @@ ltci_detection_map* fd_grft_run(const double* cube, const ltci_radar& rp, const 
     validate_radar(rp);
     check_same_params(rp, s.radar);
     if (rp.K < 16 || rp.K > 8192) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be in [16, 8192]");
-    if (rp.M > 4096) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: fd_grft supports M <= 4096");
+    if (rp.M > 1 << 20) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: fd_grft supports M <= 2^20");
     const int P = s.order;
     if (P < 1 || P > LTCI_MAX_ORDER) fail(LTCI_INVALID_ARGUMENT, "fd_grft: order must be in [1, 4]");
     unsigned long long cells = 1;

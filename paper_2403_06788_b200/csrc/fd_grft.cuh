@@ -15,7 +15,8 @@
 // the phase error is <= 2^-32 (1 + |g|) cycles.
 //
 //   K5 fd_mf_kernel       CG cells per CTA share every cube load; threads over
-//                         rows, loop over pulses; acc written [cell][K]
+//                         rows (one SFU sincos per thread, rows chained by exact
+//                         per-pulse rotors), loop over pulses; acc written [cell][K]
 //   K6 fd_fft_scan_kernel in-place mixed-radix DIF transform of PG = 16384/K
 //                         cells per CTA (the coarse-stage passes), then the
 //                         ROI scan: |v| > retain candidates, dense store,
@@ -46,82 +47,112 @@ struct FdArgs {
     PeakSlot* best;               // global argmax slot
 };
 
-constexpr int kFdThreads = 256;
-constexpr int kFdCells = 4;  // cells per MF CTA
+constexpr int kFdCells = 4;  // max cells per MF CTA (batch granularity)
+
+// MF CTA shape per K: rows per thread RPT = K / threads, cells x RPT <= 32
+// accumulators per thread (64 registers) -- more rows per thread means fewer
+// SFU sincos per term (one per thread, cell and pulse)
+__host__ __device__ constexpr int fd_threads(int K) { return K / 4 < 32 ? 32 : (K / 4 > 256 ? 256 : K / 4); }
+__host__ __device__ constexpr int fd_rpt(int K) { return K >= fd_threads(K) ? K / fd_threads(K) : 1; }
+__host__ __device__ constexpr int fd_cells(int K) { return fd_rpt(K) <= 8 ? 4 : (fd_rpt(K) <= 16 ? 2 : 1); }
 
 __device__ __forceinline__ unsigned fd_frac_u32(double cycles) {
     const double f = cycles - floor(cycles);  // [0, 1)
     return static_cast<unsigned>(static_cast<unsigned long long>(f * 4294967296.0) & 0xffffffffull);
 }
 
-// grid: ceil(c_count / kFdCells); block kFdThreads; dynamic smem 2 * kFdCells * M u32
+constexpr int kFdTile = 256;  // pulses per staged tile of per-(cell, pulse) scalars
+
+// grid: ceil(c_count / fd_cells(K)); block fd_threads(K); static smem (scalars of one pulse tile)
+//
+// Thread t owns rows r_q = t + T q (T threads).  Their wrapped indices differ
+// by the thread-independent offsets  D_q = T q  (q < K/2T)  or  T q - K, so
+//   e^{j phi(r_q)} = e^{j phi(r_0)} rho^q  (times omega once past K/2),
+// rho = e^{j 2 pi T B_m}, omega = e^{-j 2 pi K B_m}: one SFU sincos per
+// (thread, cell, pulse) instead of one per row.
 template <int K>
-__global__ void __launch_bounds__(kFdThreads) fd_mf_kernel(FdArgs a) {
-    constexpr int RPT = K >= kFdThreads ? K / kFdThreads : 1;
-    extern __shared__ unsigned s_ph[];  // [cell][m] A, then [cell][m] B
+__global__ void __launch_bounds__(fd_threads(K)) fd_mf_kernel(FdArgs a) {
+    constexpr int kFdThreads = fd_threads(K);
+    constexpr int RPT = fd_rpt(K);
+    constexpr int CPB = fd_cells(K);
+    constexpr int QH = K >= 2 * kFdThreads ? K / (2 * kFdThreads) : RPT;  // first row index past K/2
+    __shared__ unsigned sA[CPB][kFdTile], sB[CPB][kFdTile];
+    __shared__ float2 sRho[CPB][kFdTile], sRhoW[CPB][kFdTile];
     const int M = a.M;
-    unsigned* sA = s_ph;
-    unsigned* sB = s_ph + kFdCells * M;
-    const unsigned long long cell0 = static_cast<unsigned long long>(blockIdx.x) * kFdCells;
-    const int ncell = static_cast<int>(min(static_cast<unsigned long long>(kFdCells), a.c_count - cell0));
+    const unsigned long long cell0 = static_cast<unsigned long long>(blockIdx.x) * CPB;
+    const int ncell = static_cast<int>(min(static_cast<unsigned long long>(CPB), a.c_count - cell0));
 
-    for (int i = threadIdx.x; i < kFdCells * M; i += kFdThreads) {
-        const int g = i / M, m = i - g * M;
-        unsigned A = 0, B = 0;
-        if (g < ncell) {
-            // decode_motion (detectors.cpp:84-92): c_1 fastest
-            unsigned long long rem = a.c_begin + cell0 + g;
-            const double t = static_cast<double>(m + 1) * a.inv_prf;
-            double S = 0.0, tp = 1.0;
-            for (int p = 0; p < a.P; ++p) {
-                const int ip = static_cast<int>(rem % static_cast<unsigned long long>(a.count[p]));
-                rem /= static_cast<unsigned long long>(a.count[p]);
-                tp *= t;
-                S += (a.start[p] + a.step[p] * static_cast<double>(ip)) * tp;
-            }
-            A = fd_frac_u32(S * a.two_over_lambda);
-            B = fd_frac_u32(S * a.two_df_over_c);
-        }
-        sA[i] = A;
-        sB[i] = B;
-    }
-    __syncthreads();
-
-    float2 acc[kFdCells][RPT];
-    unsigned gu[RPT];
+    float2 acc[CPB][RPT];
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        const int r = threadIdx.x + q * kFdThreads;
-        gu[q] = static_cast<unsigned>(r < K / 2 ? r : r - K);
+    for (int c = 0; c < CPB; ++c)
 #pragma unroll
-        for (int c = 0; c < kFdCells; ++c) acc[c][q] = make_float2(0.f, 0.f);
-    }
+        for (int q = 0; q < RPT; ++q) acc[c][q] = make_float2(0.f, 0.f);
+    const int r0 = threadIdx.x;
+    const unsigned g0 = static_cast<unsigned>(r0 < K / 2 ? r0 : r0 - K);
     const bool live = K >= kFdThreads || threadIdx.x < K;
-    if (live) {
+
+    for (int m0 = 0; m0 < M; m0 += kFdTile) {
+        const int tm = min(kFdTile, M - m0);
+        __syncthreads();  // previous tile consumed
+        for (int i = threadIdx.x; i < CPB * kFdTile; i += kFdThreads) {
+            const int g = i / kFdTile, mm = i - g * kFdTile;
+            unsigned A = 0, B = 0;
+            if (g < ncell && mm < tm) {
+                // decode_motion (detectors.cpp:84-92): c_1 fastest
+                unsigned long long rem = a.c_begin + cell0 + g;
+                const double t = static_cast<double>(m0 + mm + 1) * a.inv_prf;
+                double S = 0.0, tp = 1.0;
+                for (int p = 0; p < a.P; ++p) {
+                    const int ip = static_cast<int>(rem % static_cast<unsigned long long>(a.count[p]));
+                    rem /= static_cast<unsigned long long>(a.count[p]);
+                    tp *= t;
+                    S += (a.start[p] + a.step[p] * static_cast<double>(ip)) * tp;
+                }
+                A = fd_frac_u32(S * a.two_over_lambda);
+                B = fd_frac_u32(S * a.two_df_over_c);
+            }
+            sA[g][mm] = A;
+            sB[g][mm] = B;
+            // exact mod-one-cycle products, then an accurate FP32 sincospi
+            float rs, rc, ws, wc;
+            sincospif(static_cast<float>(static_cast<int>(B * static_cast<unsigned>(kFdThreads))) * 4.656612873077393e-10f, &rs, &rc);  // 2^-31
+            sincospif(-static_cast<float>(static_cast<int>(B * static_cast<unsigned>(K))) * 4.656612873077393e-10f,
+                      &ws, &wc);
+            sRho[g][mm] = make_float2(rc, rs);
+            sRhoW[g][mm] = make_float2(rc * wc - rs * ws, rc * ws + rs * wc);
+        }
+        __syncthreads();
+        if (live) {
 #pragma unroll 2
-        for (int m = 0; m < M; ++m) {
-            float2 y[RPT];
+            for (int mm = 0; mm < tm; ++mm) {
+                const int m = m0 + mm;
+                float2 y[RPT];
 #pragma unroll
-            for (int q = 0; q < RPT; ++q) y[q] = __ldg(a.cube + static_cast<size_t>(m) * K + threadIdx.x + q * kFdThreads);
+                for (int q = 0; q < RPT; ++q) y[q] = __ldg(a.cube + static_cast<size_t>(m) * K + r0 + q * kFdThreads);
 #pragma unroll
-            for (int c = 0; c < kFdCells; ++c) {
-                const unsigned A = sA[c * M + m], B = sB[c * M + m];
-#pragma unroll
-                for (int q = 0; q < RPT; ++q) {
-                    const int ph = static_cast<int>(A + B * gu[q]);  // signed cycles * 2^32
+                for (int c = 0; c < CPB; ++c) {
+                    const int ph = static_cast<int>(sA[c][mm] + sB[c][mm] * g0);  // signed cycles * 2^32
                     float s, co;
                     __sincosf(static_cast<float>(ph) * 1.46291807926715968e-09f, &s, &co);  // 2 pi / 2^32
-                    acc[c][q].x = fmaf(y[q].x, co, fmaf(-y[q].y, s, acc[c][q].x));
-                    acc[c][q].y = fmaf(y[q].x, s, fmaf(y[q].y, co, acc[c][q].y));
+                    float2 z = make_float2(co, s);
+                    const float2 rho = sRho[c][mm];
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q) {
+                        if (q > 0) z = cmul(z, q == QH ? sRhoW[c][mm] : rho);
+                        acc[c][q].x = fmaf(y[q].x, z.x, fmaf(-y[q].y, z.y, acc[c][q].x));
+                        acc[c][q].y = fmaf(y[q].x, z.y, fmaf(y[q].y, z.x, acc[c][q].y));
+                    }
                 }
             }
         }
+    }
+    if (live) {
 #pragma unroll
-        for (int c = 0; c < kFdCells; ++c) {
+        for (int c = 0; c < CPB; ++c) {
             if (c < ncell) {
 #pragma unroll
                 for (int q = 0; q < RPT; ++q)
-                    a.acc[(cell0 + c) * K + threadIdx.x + q * kFdThreads] = acc[c][q];
+                    a.acc[(cell0 + c) * K + r0 + q * kFdThreads] = acc[c][q];
             }
         }
     }

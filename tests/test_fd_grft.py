@@ -135,3 +135,23 @@ def test_fd_grft_vs_reference_live():
     assert len(ours) == len(rows) > 0
     for d, r in zip(ours[:5], rows[:5]):
         assert d.flat_index == int(r[5]) and d.statistic == pytest.approx(r[0], rel=TOL)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("K,M", [(16, 64), (128, 32), (512, 16), (1024, 16), (2048, 8), (4096, 8), (8192, 4)])
+def test_fd_grft_all_sizes_vs_reference(K, M):
+    """Dense maps against the reference at every supported K (transform radix
+    plans 16 .. 16x16x16x2, rotor chains of 1 .. 32 rows per thread)."""
+    from paper_2403_06788_b200 import fd_grft, scene
+    p = RadarParams.create(3e9, 20e6, 18e6, 1000.0, M, K)
+    x = scene.to_complex64_roundtrip(scene.add_noise(np.zeros((M, K), complex), 1.0, K + M))
+    s = build_single_scale(p, 2, [Bounds(-40.0, 40.0), Bounds(-8000.0, 8000.0)], [0.5, 0.5], RangeRoi(1, K - 2))
+    s.c[0].count = min(s.c[0].count, 7)
+    s.c[1].count = min(s.c[1].count, 3)
+    opt = DetectorOptions(retain_threshold=0.0, keep_dense=True)
+    gm = fd_grft(x, p, s, opt)
+    ref = O.ref_fd(x, p, s, opt)
+    assert gm.counters == ref.counters
+    assert np.abs(gm.dense - ref.dense).max() / np.abs(ref.dense).max() <= TOL
+    assert max_rel(gm.dense, ref.dense) <= TOL
