@@ -280,6 +280,51 @@ int ltci_cuda_cube_file_write(const char *path, const ltci_cube_header *hdr, con
  * CubeFile::to_freq_cube (proj/src/cube_io.cpp:48-52). */
 int ltci_engine_run_file(ltci_engine *e, const char *path, void *stream);
 
+/* ---- batched Monte-Carlo Pd ----------------------
+ * Target / Scenario / PdPoint of proj/include/ltci/{signal_model,bench}.hpp. */
+#define LTCI_MAX_TARGETS 8
+#define LTCI_MAX_SNR 64
+typedef struct {
+    double amp[2];                      /* complex amplitude (unit scale in a Scenario) */
+    int32_t order;                      /* motion order: c[0..order] used */
+    double c[LTCI_MAX_ORDER + 1];       /* slant range c0 + c1 t + c2 t^2 + ... (MotionParams) */
+} ltci_target;
+
+typedef struct {
+    ltci_radar radar;
+    int32_t n_targets;
+    ltci_target targets[LTCI_MAX_TARGETS];  /* targets[0] is the truth */
+    int32_t n_snr;
+    double snr_db[LTCI_MAX_SNR];
+    int32_t trials;
+    double pfa, sigma2;
+    uint64_t seed;
+    int32_t n_detectors;
+    int32_t detectors[5];               /* LTCI_FD_GRFT, LTCI_DS_GRFT, LTCI_DS_KT_MFP (GPU-built kinds) */
+    int32_t P;
+    double bound_lo[LTCI_MAX_ORDER], bound_hi[LTCI_MAX_ORDER], alpha[LTCI_MAX_ORDER];
+    int32_t roi_first, roi_last;
+    int32_t keystone_taps;
+    int32_t device;
+} ltci_scenario;
+
+typedef struct {
+    double snr_db, pd;
+    int32_t trials;
+    double ci_lo, ci_hi;                /* 95 % Wilson interval (bench.cpp:60-68) */
+} ltci_pd_point;
+
+/* synthesize_cube (proj/src/signal_model.cpp:32-51) evaluated on the device in
+ * FP64; out = 2*K*M doubles, data[k + K*m] */
+int ltci_cuda_synthesize(const ltci_radar *p, int n_targets, const ltci_target *targets, double *out);
+/* add_noise (proj/src/signal_model.cpp:53-60): the splitmix64 / Box-Muller
+ * stream of GaussianRng (proj/src/rng.cpp:8-43) generated per element on the
+ * device (element i uses draws 2i+1, 2i+2 of the counter-based stream) */
+int ltci_cuda_add_noise(const double *cube, const ltci_radar *p, double sigma2, uint64_t seed, double *out);
+/* run_pd (proj/src/bench.cpp:72-124): every trial's noisy cube is generated on
+ * the device and searched there; out[d * n_snr + s] for detector d, SNR s */
+int ltci_cuda_run_pd(const ltci_scenario *sc, ltci_pd_point *out);
+
 /* Roofline denominator for the CUDA-core fine path: dense FP32 FFMA issue
  * rate of this device, measured with a register-resident FMA chain kernel
  * over all SMs (TFLOP/s, 2 flop per FFMA). */

@@ -95,6 +95,7 @@ def ref():
                                        vp, P(C.c_int)]
         lib.ref_resolve_threads.argtypes = [C.c_int]
         lib.ref_write_cube_file.argtypes = [C.c_char_p, P(A.CCubeHeader), vp]
+        lib.ref_run_pd.argtypes = [P(A.CScenario), C.c_int, P(A.CPdPoint)]
         lib.ref_build_single_scale.argtypes = [P(A.CRadar), C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
                                                C.c_int, C.c_int, P(A.CSingleSpace)]
         lib.ref_fd_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
@@ -342,3 +343,15 @@ def ref_extract_single(m: DetectionMap, gamma: float, max_out: int = 4096) -> np
     n = C.c_int(0)
     _check(lib.ref_extract_single(C.byref(cm), C.byref(s), gamma, max_out, _vp(rows), C.byref(n)), lib)
     return rows[: n.value]
+
+
+# ------------------------------------------------- run_pd (reference, C++) ---
+def ref_run_pd(sc, threads: int = 0):
+    """ltci::run_pd on a montecarlo.Scenario; list of (snr, pd, trials, lo, hi) per detector."""
+    lib = ref()
+    c = sc.to_c()
+    out = (A.CPdPoint * (max(1, len(sc.detectors) * len(sc.snr_db))))()
+    _check(lib.ref_run_pd(C.byref(c), threads or os.cpu_count() or 1, out), lib)
+    n = len(sc.snr_db)
+    return [[(o.snr_db, o.pd, o.trials, o.ci_lo, o.ci_hi) for o in out[i * n:(i + 1) * n]]
+            for i in range(len(sc.detectors))]

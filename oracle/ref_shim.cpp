@@ -579,6 +579,39 @@ int ref_extract_single(const ltci_detection_map* m, const ltci_single_space* s, 
     });
 }
 
+// run_pd (proj/src/bench.cpp:72-124) on a Scenario built field by field
+int ref_run_pd(const ltci_scenario* sc, int threads, ltci_pd_point* out) {
+    return guarded([&] {
+        R::Scenario s;
+        s.params = radar_of(sc->radar);
+        for (int t = 0; t < sc->n_targets; ++t) {
+            const ltci_target& tg = sc->targets[t];
+            std::vector<double> c(tg.c, tg.c + tg.order + 1);
+            s.targets.push_back(R::Target{R::cplx(tg.amp[0], tg.amp[1]), R::MotionParams(c)});
+        }
+        s.snr_db.assign(sc->snr_db, sc->snr_db + sc->n_snr);
+        s.trials = sc->trials;
+        s.pfa = sc->pfa;
+        s.sigma2 = sc->sigma2;
+        s.seed = sc->seed;
+        for (int d = 0; d < sc->n_detectors; ++d) s.detectors.push_back(static_cast<R::DetectorKind>(sc->detectors[d]));
+        s.P = sc->P;
+        for (int p = 0; p < sc->P; ++p) {
+            s.bounds.push_back(R::Bounds{sc->bound_lo[p], sc->bound_hi[p]});
+            s.alpha.push_back(sc->alpha[p]);
+        }
+        s.roi = R::RangeRoi{sc->roi_first, sc->roi_last};
+        s.keystone_taps = sc->keystone_taps;
+        s.threads = threads;
+        std::vector<R::PdCurve> curves = R::run_pd(s);
+        for (std::size_t d = 0; d < curves.size(); ++d)
+            for (std::size_t i = 0; i < curves[d].points.size(); ++i) {
+                const R::PdPoint& q = curves[d].points[i];
+                out[d * sc->n_snr + i] = ltci_pd_point{q.snr_db, q.pd, q.trials, q.ci_lo, q.ci_hi};
+            }
+    });
+}
+
 int ref_resolve_threads(int requested) { return R::resolve_threads(requested); }
 
 }  // extern "C"

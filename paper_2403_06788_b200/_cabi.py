@@ -76,3 +76,26 @@ class CDetection(C.Structure):
 
 class CCubeHeader(C.Structure):
     _fields_ = [("domain", C.c_int32), ("radar", CRadar), ("sigma2", C.c_double)]
+
+
+MAX_TARGETS = 8
+MAX_SNR = 64
+
+
+class CTarget(C.Structure):
+    _fields_ = [("amp", C.c_double * 2), ("order", C.c_int32), ("c", C.c_double * (MAX_ORDER + 1))]
+
+
+class CScenario(C.Structure):
+    _fields_ = [("radar", CRadar), ("n_targets", C.c_int32), ("targets", CTarget * MAX_TARGETS),
+                ("n_snr", C.c_int32), ("snr_db", C.c_double * MAX_SNR), ("trials", C.c_int32),
+                ("pfa", C.c_double), ("sigma2", C.c_double), ("seed", C.c_uint64),
+                ("n_detectors", C.c_int32), ("detectors", C.c_int32 * 5), ("P", C.c_int32),
+                ("bound_lo", C.c_double * MAX_ORDER), ("bound_hi", C.c_double * MAX_ORDER),
+                ("alpha", C.c_double * MAX_ORDER), ("roi_first", C.c_int32), ("roi_last", C.c_int32),
+                ("keystone_taps", C.c_int32), ("device", C.c_int32)]
+
+
+class CPdPoint(C.Structure):
+    _fields_ = [("snr_db", C.c_double), ("pd", C.c_double), ("trials", C.c_int32), ("ci_lo", C.c_double),
+                ("ci_hi", C.c_double)]

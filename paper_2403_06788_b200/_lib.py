@@ -23,7 +23,7 @@ EXPORTS = (
     "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path",
     "ltci_engine_work", "ltci_engine_run_file", "ltci_cuda_fd_grft", "ltci_cuda_extract_detections_single",
     "ltci_cuda_extract_detections", "ltci_cuda_cube_file_info", "ltci_cuda_cube_file_read",
-    "ltci_cuda_cube_file_write", "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
+    "ltci_cuda_cube_file_write", "ltci_cuda_synthesize", "ltci_cuda_add_noise", "ltci_cuda_run_pd", "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
 )
 
 _lib = None
@@ -95,6 +95,9 @@ def load():
     lib.ltci_cuda_cube_file_read.argtypes = [C.c_char_p, P(A.CCubeHeader), vp, C.c_uint64]
     lib.ltci_cuda_cube_file_write.argtypes = [C.c_char_p, P(A.CCubeHeader), vp]
     lib.ltci_engine_run_file.argtypes = [vp, C.c_char_p, vp]
+    lib.ltci_cuda_synthesize.argtypes = [P(A.CRadar), C.c_int, P(A.CTarget), vp]
+    lib.ltci_cuda_add_noise.argtypes = [vp, P(A.CRadar), C.c_double, C.c_uint64, vp]
+    lib.ltci_cuda_run_pd.argtypes = [P(A.CScenario), P(A.CPdPoint)]
     lib.ltci_cuda_fd_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
     lib.ltci_cuda_extract_detections_single.argtypes = [P(A.CDetectionMap), P(A.CSingleSpace), C.c_double,
                                                         P(A.CDetection), C.c_int, P(C.c_int)]

@@ -206,6 +206,38 @@ int extract_impl(const Ctx& x, double gamma, ltci_detection* out, int max_out, i
 
 }  // namespace
 
+// detection_success (proj/src/bench.cpp:30-46): some retained cell estimates the
+// truth within one cell on every axis (cell sizes of estimate_cell_sizes,
+// detection.cpp:55-79).  Used by the Monte-Carlo driver (pd.cu).
+bool ltcib_detection_success(const ltci_detection_map* map, const ltci_dual_space* ds, const ltci_single_space* ss,
+                             const ltci_ambiguity* amb, const ltci_target& truth) {
+    const ltci_radar& r = ds ? ds->radar : ss->radar;
+    const double va = (kC / r.fc) * r.PRF / 2.0;
+    Ctx x{map, ds, ss, amb, r.M, kC / (2.0 * r.fs), va};
+    const double cs_range = x.dR;
+    double cs_vel = 0.0, cs_acc = 0.0;
+    if (map->kind == LTCI_FD_GRFT) {
+        cs_vel = ss->c[0].step;
+        if (ss->order >= 2) cs_acc = ss->c[1].step;
+    } else if (map->kind == LTCI_DS_GRFT) {
+        cs_vel = (va / r.M) / ds->kappa;
+        if (ds->order >= 2) cs_acc = ds->fine[1].step;
+    } else {
+        cs_vel = va / r.M;
+        cs_acc = ds->fine[1].step;
+    }
+    for (uint64_t i = 0; i < map->n_candidates; ++i) {
+        const ltci_detection d =
+            from_cell(x, decode(*map, map->cand_index[i]), map->cand_value[2 * i], map->cand_value[2 * i + 1],
+                      map->cand_index[i]);
+        if (std::abs(d.c[0] - truth.c[0]) > cs_range * 1.0001) continue;
+        if (truth.order >= 1 && std::abs(d.c[1] - truth.c[1]) > cs_vel * 1.0001) continue;
+        if (truth.order >= 2 && d.n_coef - 1 >= 2 && std::abs(d.c[2] - truth.c[2]) > cs_acc * 1.0001) continue;
+        return true;
+    }
+    return false;
+}
+
 extern "C" int ltci_cuda_extract_detections(const ltci_detection_map* map, const ltci_dual_space* space,
                                             const ltci_ambiguity* amb, double gamma, ltci_detection* out,
                                             int max_out, int* n_out) {

@@ -1011,8 +1011,8 @@ void fd_launch(const FdArgs& a, cudaStream_t st) {
     }
 }
 
-ltci_detection_map* fd_grft_run(const double* cube, const ltci_radar& rp, const ltci_single_space& s,
-                                const ltci_options* opt) {
+ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const ltci_radar& rp,
+                                const ltci_single_space& s, const ltci_options* opt) {
     validate_radar(rp);
     check_same_params(rp, s.radar);
     if (rp.K < 16 || rp.K > 8192) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be in [16, 8192]");
@@ -1061,11 +1061,14 @@ ltci_detection_map* fd_grft_run(const double* cube, const ltci_radar& rp, const 
     auto& cand = w.cand;
     auto& ccount = w.ccount;
     auto& best = w.best;
-    f64.ensure(n);
-    c64.ensure(n);
-    CK(cudaMemcpyAsync(f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice, st));
-    f64_to_c64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(f64.p, c64.p, n);
-    CK(cudaGetLastError());
+    if (!d_cube) {
+        f64.ensure(n);
+        c64.ensure(n);
+        CK(cudaMemcpyAsync(f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice, st));
+        f64_to_c64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(f64.p, c64.p,
+                                                                                                          n);
+        CK(cudaGetLastError());
+    }
 
     size_t free_b = 0, total_b = 0;
     if (keep_dense) {
@@ -1084,7 +1087,7 @@ ltci_detection_map* fd_grft_run(const double* cube, const ltci_radar& rp, const 
     best.ensure(1);
 
     FdArgs a{};
-    a.cube = c64.p;
+    a.cube = d_cube ? d_cube : c64.p;
     a.acc = acc.p;
     a.K = K;
     a.M = M;
@@ -1175,6 +1178,17 @@ ltci_detection_map* fd_grft_run(const double* cube, const ltci_radar& rp, const 
 
 }  // namespace
 
+// fd_grft on a device-resident complex64 cube (the Monte-Carlo driver, pd.cu);
+// throws ltcib::Status-like errors through the same guarded() wrappers
+ltci_detection_map* ltcib_fd_grft_device(const float2* d_cube, const ltci_radar& rp, const ltci_single_space& s,
+                                         const ltci_options* opt) {
+    try {
+        return fd_grft_run(nullptr, d_cube, rp, s, opt);
+    } catch (const Error& e) {
+        throw ltcib::CubeError(e.code, e.msg);  // status-carrying error across translation units
+    }
+}
+
 extern "C" {
 
 int ltci_cuda_measure_fp32_peak(int device, double* tflops) {
@@ -1221,7 +1235,7 @@ int ltci_cuda_fd_grft(const double* cube, const ltci_radar* cube_params, const l
                       const ltci_options* opt, ltci_detection_map** out) {
     return guarded([&] {
         if (!cube || !cube_params || !space || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
-        *out = fd_grft_run(cube, *cube_params, *space, opt);
+        *out = fd_grft_run(cube, nullptr, *cube_params, *space, opt);
     });
 }
 
