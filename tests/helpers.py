@@ -81,3 +81,41 @@ def check_peaks(gi, gv, ri, rv, tol=TOL, value_at=None):
         alt = abs(value_at(int(gi[r])))
         assert abs(alt - abs(rv[r])) <= tol * abs(rv[r]), f"row {r}: index {gi[r]} vs {ri[r]} is not a tie"
     return len(bad)
+
+
+def oracle_cell(x, params, space, idx, variant=0, amb=None):
+    """FP64 oracle value of one dual-scale flat cell: the C restatement run on
+    the space restricted to that cell's coarse cell and ROI row (full fine and
+    Doppler axes), read at the cell's (fine, Doppler) position.  Size-independent:
+    lets full BASELINE-size GPU maps be checked at sampled cells."""
+    import copy
+
+    import oracle as O
+    from paper_2403_06788_b200.configs import doppler_window
+    from paper_2403_06788_b200.model import AmbiguitySpace, DetectorOptions, Grid, RangeRoi
+    s = space
+    D = doppler_window(params, s)[1] if variant == 0 else params.M
+    R = s.roi.count()
+    F = int(np.prod([g.count for g in s.fine[1:]])) if s.order() > 1 else 1
+    if variant == 1:
+        F = s.fine[1].count
+    jj = idx % D
+    r = (idx // D) % R
+    f = (idx // (D * R)) % F
+    c = idx // (D * R * F)
+    sl = copy.deepcopy(s)
+    sl.roi = RangeRoi(s.roi.first + r, s.roi.first + r)
+    a2 = amb
+    if variant == 0:
+        rem = c
+        for i in reversed(range(s.order())):
+            ci = rem % s.coarse[i].count
+            rem //= s.coarse[i].count
+            sl.coarse[i] = Grid(s.coarse[i].value(ci), s.coarse[i].step, 1)
+    else:
+        ci = c % s.coarse[1].count
+        q = amb.q_min + c // s.coarse[1].count
+        sl.coarse[1] = Grid(s.coarse[1].value(ci), s.coarse[1].step, 1)
+        a2 = AmbiguitySpace(q, q)
+    m = O.port_ds(x, params, sl, DetectorOptions(retain_threshold=-1.0, keep_dense=True), variant, a2)
+    return complex(m.dense[f * D + jj])
