@@ -12,7 +12,7 @@ import os
 from . import _cabi as A
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libltci_cuda.so")
+LIB_PATH = os.environ.get("LTCI_LIB_PATH") or os.path.join(LIB_DIR, "libltci_cuda.so")  # override: experiments
 DROPIN_PATH = os.path.join(LIB_DIR, "libltci_b200.so")
 
 # Every symbol include/ltci_cuda.h declares.
