@@ -409,9 +409,14 @@ def main():
         else:
             per_launch_flops = coarse * rows_here * fine_cells * fft_flops_per_row_cell(p.M, D)
             achieved = per_launch_flops / fine_s / 1e12
-            roof = {"bound": "fp32", "kernel": "fine_fft_kernel (K2b+K3, CUDA cores)",
+            tm = p.M == 1024
+            roof = {"bound": "fp32",
+                    "kernel": "fine_fft_tm_kernel (K2b+K3, CUDA cores, TMEM-resident rows)" if tm
+                    else "fine_fft_kernel (K2b+K3, CUDA cores)",
                     "achieved": achieved, "peak": fp32.value, "unit": "TFLOP/s",
-                    "frac": achieved / fp32.value if fp32.value else None, "traffic": None,
+                    "frac": achieved / fp32.value if fp32.value else None,
+                    "traffic": _ncu_traffic(args.config, "fine_fft_tm_kernel<0>") if tm else None,
+                    "traffic_source": "profiles/r01_ncu_c1.json (ncu --set full, bytes per launch)",
                     "peak_source": "measured in-run FFMA chain microbenchmark (ltci_cuda_measure_fp32_peak)",
                     "algorithmic": "per (row, fine cell): 6M chirp + 5M log2M FFT + 3D |Y|^2 flop",
                     "dense_equiv_tflops": 8.0 * integ / fine_s / 1e12}

@@ -104,3 +104,7 @@ def test_fine_path_selection_is_honoured():
     e = Engine(w3.params, w3.space, 1, w3.amb, DetectorOptions())
     assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE  # full Doppler axis -> FFT
     e.close()
+    w1 = config(1)
+    e = Engine(w1.params, w1.space, opt=DetectorOptions())
+    assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE  # M = 1024: TMEM-resident FFT path
+    e.close()
