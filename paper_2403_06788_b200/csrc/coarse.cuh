@@ -48,11 +48,12 @@ struct CoarseArgs {
 //   pass 1     global loads (all in flight) -> fractional ramp -> DFT16 ->
 //              twiddle -> shared
 //   middle     shared -> DFT16 -> twiddle -> shared (same positions)
-//   last       shared -> per-pulse rotation -> DFT_R -> preDFM -> global
+//   last       shared -> preDFM -> DFT_R -> per-pulse rotation -> global
 // The last pass produces, per (pulse p, row group g), the R rows g + G t
 // (G = K / R) directly: the integer part of the pulse's shift becomes a
-// rotation of the output index, folded into an input pre-twiddle, so lanes
-// p = 0..PG-1 of a warp write the same row (PG contiguous pulses).
+// rotation of the output index (an exact register barrel shift after the
+// DFT), so lanes p = 0..PG-1 of a warp write the same row (PG contiguous
+// pulses) and every value depends only on its absolute bin.
 constexpr int kCoarseThreads = 512;
 constexpr int kCoarseSamples = 16384;
 
@@ -127,12 +128,23 @@ __device__ __forceinline__ void coarse_last_pass(const CoarseArgs& a, const floa
         float2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = src[cpad(pos0 + r)];
-        // output t <- bin kl + G (t + c): pre-twiddle by w_R^{c r}, times preDFM
-        if constexpr (R > 1) twiddle_pow<R>(v, c, R);
         const float2 pre = make_float2(s_pre[p].x * sc, s_pre[p].y * sc);
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = cmul(v[r], pre);
         dft_reg<R>(v);
+        // output t <- bin kl + G (t + c): an exact barrel rotation of the R outputs
+        // (no arithmetic, so a row's value depends only on its absolute bin and
+        // range-cell shards reproduce the 1-GPU map bit for bit)
+#pragma unroll
+        for (int b = 1; b < R; b <<= 1) {
+            if (c & b) {
+                float2 w[R];
+#pragma unroll
+                for (int t = 0; t < R; ++t) w[t] = v[(t + b) & (R - 1)];
+#pragma unroll
+                for (int t = 0; t < R; ++t) v[t] = w[t];
+            }
+        }
 #pragma unroll
         for (int t = 0; t < R; ++t) {
             const int n = g + G * t;

@@ -97,3 +97,31 @@ def test_c4_one_cpi_full_size():
     x = scene.to_complex64_roundtrip(w.cube(cpi=5))
     gamma = detection_threshold(w.params, w.sigma2, 1e-6)
     _cross_and_oracle(w, x, gamma, samples=6, seed=4)
+
+
+def test_c1_range_shards_merge_bit_exactly():
+    """C1 on the TMEM-resident FFT path split into 3 uneven range-cell shards
+    (the multi-GPU partition, one engine per GPU) merges to the 1-GPU map
+    bit-exactly; parallel.merge_rank_maps is the merge the NCCL gather feeds."""
+    from paper_2403_06788_b200.parallel import merge_rank_maps, shard_rows
+    w = config(1)
+    x = scene.to_complex64_roundtrip(w.cube())
+    gamma = detection_threshold(w.params, w.sigma2, 1e-6)
+    opt = DetectorOptions(retain_threshold=gamma)
+    full = Engine(w.params, w.space, opt=opt)
+    assert full.fine_path()[0] == A.FINE_FFT_CUDA_CORE
+    full.run_host(x)
+    a = full.result()
+    full.close()
+    R = w.space.roi.count()
+    maps = []
+    for rank in range(3):
+        lo, hi = shard_rows(R, 3, rank)
+        e = Engine(w.params, w.space, opt=opt, row_begin=lo, row_end=hi)
+        e.run_host(x)
+        maps.append(e.result())
+        e.close()
+    m = merge_rank_maps(maps)
+    assert np.array_equal(m.peak_index, a.peak_index) and np.array_equal(m.peak_value, a.peak_value)
+    assert np.array_equal(m.cand_index, a.cand_index) and np.array_equal(m.cand_value, a.cand_value)
+    assert m.argmax == a.argmax
