@@ -21,6 +21,7 @@ cpu_baseline  (rank 0, N = 1) the reference's own ds_grft/ds_kt_mfp compiled
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -59,6 +60,9 @@ def parse():
     ap.add_argument("--coarse-slice", type=int, default=0,
                     help="restrict the coarse-velocity axis (rate measurement of configs too large for one step)")
     ap.add_argument("--coarse-rest", type=int, default=0, help="with --coarse-slice: restrict the other coarse axes")
+    ap.add_argument("--shard", default="auto", choices=["auto", "rows", "coarse"],
+                    help="one-CPI partition across ranks: coarse cells (no replicated work; default when every "
+                         "rank gets one) or range cells")
     return ap.parse_args()
 
 
@@ -258,16 +262,32 @@ def main():
     opt = DetectorOptions(retain_threshold=gamma, fine_path=fine_path, device=local)
     R = s.roi.count()
     cpis = w.cpis
+    if w.variant == 0:
+        n_coarse = int(np.prod([g.count for g in s.coarse]))
+    else:
+        n_coarse = w.amb.count() * s.coarse[1].count
+    shard = args.shard
+    if shard == "auto":
+        shard = "coarse" if n_coarse >= ws else "rows"
+    c_lo, c_hi = 0, -1
     if cpis > 1:
         # CPI-level data parallelism (configs[4]): each rank streams its CPIs, full ROI
         lo, hi = 0, R
         my_cpis = list(range(rank * cpis // ws, (rank + 1) * cpis // ws))
+        shard = "cpis"
+    elif shard == "coarse":
+        # one CPI sharded over coarse cells (SURVEY.md 8(e) alternative): every rank
+        # searches its coarse cells over every ROI row, nothing replicated
+        from paper_2403_06788_b200.parallel import shard_coarse
+        lo, hi = 0, R
+        c_lo, c_hi = shard_coarse(n_coarse, ws, rank)
+        my_cpis = [0]
     else:
         # one CPI sharded over range start cells
         lo, hi = rank * R // ws, (rank + 1) * R // ws
         my_cpis = [0]
     log("engine")
-    eng = Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi)
+    eng = Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi, coarse_begin=c_lo, coarse_end=c_hi)
     log("synthesising cubes")
     hyp, integ = eng.work()
 
@@ -279,11 +299,23 @@ def main():
     sptr = stream.cuda_stream
     peak_ptr, n_rows = eng.peaks_device()
     peaks = torch.as_tensor(_CAI(peak_ptr, (n_rows, 4), "<u4"), device=dev)
-    gathered = torch.empty((ws * (R // ws + 1), 4), dtype=torch.int32, device=dev) if ws > 1 else None
     per_cpi_peaks = torch.empty((len(my_cpis), n_rows, 4), dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    if ws > 1 and shard == "coarse":
+        gathered = torch.empty((ws, R, 4), dtype=torch.int32, device=dev)
+        merged = torch.empty((R, 4), dtype=torch.int32, device=dev)
+    elif ws > 1:
+        gathered = torch.empty((ws * (R // ws + 1), 4), dtype=torch.int32, device=dev)
 
     def gather_peaks():
-        if ws > 1 and cpis == 1:
+        if ws > 1 and shard == "coarse":
+            # every rank holds a peak per row: NCCL all-gather of the 16-byte records,
+            # then the per-row max on the device with the kernels' tie-break
+            dist.all_gather_into_tensor(gathered, peaks.view(torch.int32))
+            _lib.raise_for(lib.ltci_cuda_merge_peaks(ctypes.c_void_p(gathered.data_ptr()), ws, R,
+                                                     ctypes.c_void_p(merged.data_ptr()), ctypes.c_void_p(sptr)),
+                           lib)
+        elif ws > 1 and cpis == 1:
             # slices differ by at most one row: pad to a common length
             pad = torch.zeros((R // ws + 1, 4), dtype=torch.int32, device=dev)
             pad[:n_rows].copy_(peaks.view(torch.int32))
@@ -384,6 +416,8 @@ def main():
             coarse = w.amb.count() * s.coarse[1].count
             fine_cells = s.fine[1].count
         rows_here = (hi - lo)
+        if shard == "coarse" and ws > 1:
+            coarse = c_hi - c_lo  # this rank's coarse cells (every row)
         hbm = peaks_json.get("hbm_gbs", 6650.0)
         x_bytes = 8.0 * coarse * rows_here * p.M + 8.0 * p.K * p.M
         coarse_fft_flops = coarse * p.M * (5.0 * p.K * np.log2(p.K) + 8.0 * p.K)
@@ -445,7 +479,8 @@ def main():
             "config": {"workload": w.name, "config_index": args.config, "K": p.K, "M": p.M, "cpis": cpis,
                        "hypotheses_per_cpi": w.hypotheses(), "integrations_per_step": total_integ,
                        "integrations_per_s_G": value,
-                       "parallelism": ("CPI shards" if cpis > 1 else "range-cell shards") + f" x{ws}",
+                       "parallelism": {"cpis": "CPI shards", "coarse": "coarse-cell shards",
+                                       "rows": "range-cell shards"}[shard] + f" x{ws}",
                        "retain_threshold": gamma, "pfa": args.pfa,
                        "l2": "flushed between steps (512 MiB write, untimed); X stream >> L2",
                        "fine_path": args.fine_path + (" -> tcgen05" if use_tc else " -> cuda-core fft")},

@@ -250,6 +250,15 @@ int ltci_engine_set_timing(ltci_engine *e, int enable);
 int ltci_engine_fine_path(ltci_engine *e, int32_t *path, int32_t *terms);
 /* hypotheses (cells) and integrations covered by this engine's row slice */
 int ltci_engine_work(ltci_engine *e, uint64_t *hypotheses, uint64_t *integrations);
+/* extension: restrict the engine to coarse cells [c_begin, c_end) of the plan
+ * (coarse-cell sharding: each GPU searches its coarse cells over every ROI row,
+ * nothing is replicated; flat indices stay global; c_end = UINT64_MAX means
+ * the last coarse cell).  Per-row peaks of the
+ * shards combine with ltci_cuda_merge_peaks, candidates by concatenation. */
+int ltci_engine_set_coarse_slice(ltci_engine *e, uint64_t c_begin, uint64_t c_end);
+/* per-row best of n_maps device peak-slot arrays ({f32 re, f32 im, u64 flat},
+ * n_maps x n_rows, map-major) with the kernels' own magnitude and tie-break */
+int ltci_cuda_merge_peaks(const void *d_slots, int n_maps, int n_rows, void *d_out, void *stream);
 
 /* ---- cube file container ------------------------
  * The reference's "LTCI" little-endian container (proj/include/ltci/cube_io.hpp:

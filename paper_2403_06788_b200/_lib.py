@@ -21,7 +21,7 @@ EXPORTS = (
     "ltci_cuda_mgift", "ltci_cuda_gft", "ltci_cuda_detection_threshold", "ltci_engine_create",
     "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
     "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path",
-    "ltci_engine_work", "ltci_engine_run_file", "ltci_cuda_fd_grft", "ltci_cuda_extract_detections_single",
+    "ltci_engine_work", "ltci_engine_run_file", "ltci_engine_set_coarse_slice", "ltci_cuda_merge_peaks", "ltci_cuda_fd_grft", "ltci_cuda_extract_detections_single",
     "ltci_cuda_extract_detections", "ltci_cuda_cube_file_info", "ltci_cuda_cube_file_read",
     "ltci_cuda_cube_file_write", "ltci_cuda_synthesize", "ltci_cuda_add_noise", "ltci_cuda_run_pd", "ltci_cuda_measure_fp32_peak", "ltci_cuda_last_error", "ltci_cuda_version",
 )
@@ -95,6 +95,8 @@ def load():
     lib.ltci_cuda_cube_file_read.argtypes = [C.c_char_p, P(A.CCubeHeader), vp, C.c_uint64]
     lib.ltci_cuda_cube_file_write.argtypes = [C.c_char_p, P(A.CCubeHeader), vp]
     lib.ltci_engine_run_file.argtypes = [vp, C.c_char_p, vp]
+    lib.ltci_engine_set_coarse_slice.argtypes = [vp, C.c_uint64, C.c_uint64]
+    lib.ltci_cuda_merge_peaks.argtypes = [vp, C.c_int, C.c_int, vp, vp]
     lib.ltci_cuda_synthesize.argtypes = [P(A.CRadar), C.c_int, P(A.CTarget), vp]
     lib.ltci_cuda_add_noise.argtypes = [vp, P(A.CRadar), C.c_double, C.c_uint64, vp]
     lib.ltci_cuda_run_pd.argtypes = [P(A.CScenario), P(A.CPdPoint)]

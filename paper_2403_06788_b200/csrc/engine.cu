@@ -523,6 +523,8 @@ struct ltci_engine {
     DevBuf<float2> htab;
     bool htab_ready = false;
     CUtensorMap tm_hi{}, tm_lo{};
+    // coarse-cell slice searched by this engine (coarse-cell sharding across GPUs)
+    unsigned long long c_lo = 0, c_hi = ~0ull;
     // candidate assembly on the device (radix sort by flat index + recentring)
     DevBuf<unsigned long long> ck0, ck1;
     DevBuf<float2> cv0, cv1;
@@ -722,8 +724,9 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
         }
         ta.htab = e->htab.p;
     }
-    for (unsigned long long c0 = 0; c0 < pl.coarse_cells; c0 += e->batch) {
-        const unsigned long long cc = std::min<unsigned long long>(e->batch, pl.coarse_cells - c0);
+    const unsigned long long c_end = std::min(e->c_hi, pl.coarse_cells);
+    for (unsigned long long c0 = e->c_lo; c0 < c_end; c0 += e->batch) {
+        const unsigned long long cc = std::min<unsigned long long>(e->batch, c_end - c0);
         ca.c_begin = c0;
         ca.c_count = static_cast<int>(cc);
         int evc = -1;
@@ -1198,6 +1201,26 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
 
 }  // namespace
 
+// Per-row best over several peak-slot arrays (coarse-cell shards): the same
+// magnitude (mag2f) and lowest-flat-index tie-break as the kernels' CAS publish.
+__global__ void merge_peaks_kernel(const PeakSlot* __restrict__ in, int n_maps, int n_rows,
+                                   PeakSlot* __restrict__ out) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+        PeakSlot b = in[r];
+        float bm = b.idx == ~0ull ? -1.0f : mag2f(b.re, b.im);
+        for (int k = 1; k < n_maps; ++k) {
+            const PeakSlot c = in[static_cast<size_t>(k) * n_rows + r];
+            if (c.idx == ~0ull) continue;
+            const float cm = mag2f(c.re, c.im);
+            if (cm > bm || (cm == bm && c.idx < b.idx)) {
+                b = c;
+                bm = cm;
+            }
+        }
+        out[r] = b;
+    }
+}
+
 // fd_grft on a device-resident complex64 cube (the Monte-Carlo driver, pd.cu);
 // throws ltcib::Status-like errors through the same guarded() wrappers
 ltci_detection_map* ltcib_fd_grft_device(const float2* d_cube, const ltci_radar& rp, const ltci_single_space& s,
@@ -1583,9 +1606,32 @@ int ltci_engine_work(ltci_engine* e, uint64_t* hypotheses, uint64_t* integration
     return guarded([&] {
         if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
         const Plan& pl = e->pl;
-        const unsigned long long H = pl.coarse_cells * pl.fine_cells * pl.R_slice * pl.D;
+        const unsigned long long cc = std::min(e->c_hi, pl.coarse_cells) - e->c_lo;
+        const unsigned long long H = cc * pl.fine_cells * pl.R_slice * pl.D;
         if (hypotheses) *hypotheses = H;
         if (integrations) *integrations = H * static_cast<unsigned long long>(pl.rp.M);
+    });
+}
+
+int ltci_engine_set_coarse_slice(ltci_engine* e, uint64_t c_begin, uint64_t c_end) {
+    return guarded([&] {
+        if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        if (c_end == ~0ull) c_end = e->pl.coarse_cells;  // "to the end"
+        if (c_begin >= c_end || c_end > e->pl.coarse_cells)
+            fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: coarse slice must satisfy 0 <= begin < end <= coarse cells");
+        e->c_lo = c_begin;
+        e->c_hi = c_end;
+    });
+}
+
+int ltci_cuda_merge_peaks(const void* d_slots, int n_maps, int n_rows, void* d_out, void* stream) {
+    return guarded([&] {
+        if (!d_slots || !d_out || n_maps < 1 || n_rows < 0) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad merge");
+        if (n_rows == 0) return;
+        const int blocks = std::min(148 * 4, (n_rows + 255) / 256);
+        merge_peaks_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            static_cast<const PeakSlot*>(d_slots), n_maps, n_rows, static_cast<PeakSlot*>(d_out));
+        CK(cudaGetLastError());
     });
 }
 

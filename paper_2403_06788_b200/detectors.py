@@ -127,7 +127,7 @@ class Engine:
 
     def __init__(self, params: RadarParams, space: DualScaleSpace, variant: int = A.VARIANT_GRFT,
                  amb: Optional[AmbiguitySpace] = None, opt: Optional[DetectorOptions] = None,
-                 row_begin: int = 0, row_end: int = -1):
+                 row_begin: int = 0, row_end: int = -1, coarse_begin: int = 0, coarse_end: int = -1):
         self._lib = _lib.load()
         self.params, self.space, self.variant, self.amb = params, space, variant, amb
         self.opt = opt or DetectorOptions()
@@ -138,6 +138,13 @@ class Engine:
                                           C.byref(o), row_begin, row_end, C.byref(h))
         _lib.raise_for(rc, self._lib)
         self._h = h
+        if coarse_begin != 0 or coarse_end != -1:
+            self.set_coarse_slice(coarse_begin, coarse_end)
+
+    def set_coarse_slice(self, c_begin: int, c_end: int):
+        """Search only coarse cells [c_begin, c_end) (coarse-cell sharding; flat indices stay global)."""
+        _lib.raise_for(self._lib.ltci_engine_set_coarse_slice(self._h, c_begin, c_end if c_end >= 0 else (1 << 64) - 1),
+                       self._lib)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -1,4 +1,4 @@
-"""Multi-GPU range-cell sharding.
+"""Multi-GPU sharding: range cells or coarse cells.
 
 Every (coarse cell, ROI row) output of the cascade is independent, so ranks
 own contiguous slices of ROI rows (``shard_rows``): each replicates the echo,
@@ -15,6 +15,15 @@ reduces into its own per-cell peak records.  The only exchange is gathering:
 The collectives run through ``torch.distributed`` (NCCL between GPUs; gloo in
 the CPU tests).  ``merge_rank_maps`` is the deterministic host-side merge used
 by both; results are bit-identical for any rank count.
+
+Coarse-cell sharding (``shard_coarse``, SURVEY.md §8(e) "Alternative") is the
+partition that scales: each rank searches a contiguous slice of coarse cells
+over every ROI row, so no work is replicated (range sharding repeats the
+K-point coarse transforms on every rank: 2.9 ms against 28 ms of fine work per
+rank at C1 on 8 GPUs, a 4.8x ceiling).  The exchange becomes a per-row max:
+every rank holds a peak for every row, combined with the kernels' own
+magnitude and lowest-index tie-break (``ltci_cuda_merge_peaks`` on the device;
+``merge_coarse_maps`` on the host), and candidates concatenate.
 """
 from __future__ import annotations
 
@@ -30,6 +39,13 @@ def shard_rows(R: int, world: int, rank: int) -> Tuple[int, int]:
     if world < 1 or not 0 <= rank < world:
         raise ValueError("shard_rows: bad world/rank")
     return rank * R // world, (rank + 1) * R // world
+
+
+def shard_coarse(C: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous [lo, hi) slice of C coarse cells for ``rank`` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world or C < world:
+        raise ValueError("shard_coarse: need 1 <= world <= coarse cells and a valid rank")
+    return rank * C // world, (rank + 1) * C // world
 
 
 def _mag2_f32(v: np.ndarray) -> np.ndarray:
@@ -71,9 +87,59 @@ def merge_rank_maps(maps: Sequence[DetectionMap], full_counters: Optional[tuple]
     return out
 
 
+def merge_coarse_maps(maps: Sequence[DetectionMap], full_counters: Optional[tuple] = None) -> DetectionMap:
+    """Merge per-rank maps of a coarse-cell partition (every map covers every
+    row): per-row best (magnitude desc, flat index asc), candidates concatenated
+    and sorted.  Host-side: magnitudes of the recentred FP64 values; the bench
+    path merges the raw FP32 slots on the device (``ltci_cuda_merge_peaks``)."""
+    if not maps:
+        raise ValueError("merge_coarse_maps: no maps")
+    base = maps[0]
+    R = base.peak_index.size
+    if any(m.peak_index.size != R for m in maps):
+        raise ValueError("merge_coarse_maps: every map must cover the same rows")
+    out = DetectionMap(kind=base.kind, params=base.params, axes=list(base.axes),
+                       counters=full_counters if full_counters is not None else base.counters,
+                       retain_threshold=base.retain_threshold, dual=base.dual, amb=base.amb,
+                       doppler_first=base.doppler_first)
+    idx = np.stack([m.peak_index for m in maps])          # (ranks, R)
+    val = np.stack([m.peak_value for m in maps])
+    mag = np.where(idx == np.uint64(0xFFFFFFFFFFFFFFFF), -1.0, np.abs(val))
+    best = np.zeros(R, np.int64)
+    for k in range(1, len(maps)):
+        better = (mag[k] > mag[best, np.arange(R)]) | ((mag[k] == mag[best, np.arange(R)]) &
+                                                        (idx[k] < idx[best, np.arange(R)]))
+        best = np.where(better, k, best)
+    out.peak_index = idx[best, np.arange(R)].copy()
+    out.peak_value = val[best, np.arange(R)].copy()
+    ci = np.concatenate([m.cand_index for m in maps])
+    cv = np.concatenate([m.cand_value for m in maps])
+    order = np.argsort(ci, kind="stable")
+    out.cand_index, out.cand_value = ci[order], cv[order]
+    k = argmax_total_order(out.peak_index, out.peak_value)
+    if k >= 0:
+        out.argmax = int(out.peak_index[k])
+        out.argmax_value = complex(out.peak_value[k])
+    return out
+
+
+def gather_coarse_map(local: DetectionMap, group=None, device=None) -> Optional[DetectionMap]:
+    """Coarse-cell partition: all-gather every rank's per-row peaks and
+    candidates; rank 0 returns the merged map (``merge_coarse_maps``)."""
+    maps = _gather_maps(local, group, device)
+    return merge_coarse_maps(maps, local.counters) if maps is not None else None
+
+
 def gather_map(local: DetectionMap, group=None, device=None) -> Optional[DetectionMap]:
-    """All-gather every rank's peaks and candidates; rank 0 returns the merged
-    map, other ranks return None.  Works with NCCL (device tensors) and gloo."""
+    """Range-cell partition: all-gather every rank's peaks and candidates;
+    rank 0 returns the merged map, other ranks None.  NCCL or gloo."""
+    maps = _gather_maps(local, group, device)
+    return merge_rank_maps(maps, local.counters) if maps is not None else None
+
+
+def _gather_maps(local: DetectionMap, group=None, device=None) -> Optional[List[DetectionMap]]:
+    """All-gather every rank's peaks and candidates; rank 0 gets the list of
+    rank maps, other ranks None.  Works with NCCL (device tensors) and gloo."""
     import torch
     import torch.distributed as dist
 
@@ -117,7 +183,7 @@ def gather_map(local: DetectionMap, group=None, device=None) -> Optional[Detecti
         m.peak_index, m.peak_value = unpack(pg[r])
         m.cand_index, m.cand_value = unpack(cg[r])
         maps.append(m)
-    return merge_rank_maps(maps, local.counters)
+    return maps
 
 
 def split_map_by_rows(full: DetectionMap, R: int, D: int, world: int) -> List[DetectionMap]:
@@ -136,5 +202,39 @@ def split_map_by_rows(full: DetectionMap, R: int, D: int, world: int) -> List[De
         m.cand_value = full.cand_value[sel].copy()
         k = argmax_total_order(m.peak_index, m.peak_value)
         m.argmax, m.argmax_value = int(m.peak_index[k]), complex(m.peak_value[k])
+        out.append(m)
+    return out
+
+
+def split_map_by_coarse(full: DetectionMap, C: int, world: int) -> List[DetectionMap]:
+    """Test helper: the per-rank maps a coarse-sharded run produces, cut from a
+    full map that kept its dense statistic (per-row best over the rank's coarse
+    cells, ties to the lowest flat index; candidates of those cells)."""
+    if not full.dense_stored:
+        raise ValueError("split_map_by_coarse: needs a dense map")
+    H = full.dense.size
+    per_c = H // C                      # flat = c * per_c + rest, rest = (f*R + r)*D + jj
+    R = full.peak_index.size
+    D = full.axes[-1].size
+    flat = np.arange(H, dtype=np.uint64)
+    row = ((flat // np.uint64(D)) % np.uint64(R)).astype(np.int64)
+    mag = np.abs(full.dense)
+    out = []
+    for rank in range(world):
+        lo, hi = shard_coarse(C, world, rank)
+        sel = slice(lo * per_c, hi * per_c)
+        m = DetectionMap(kind=full.kind, params=full.params, axes=list(full.axes), counters=full.counters,
+                         retain_threshold=full.retain_threshold, dual=full.dual, amb=full.amb,
+                         doppler_first=full.doppler_first)
+        # per-row best: sort by (row, -mag, flat) and take the first of each row
+        r_s, m_s, f_s = row[sel], mag[sel], flat[sel]
+        order = np.lexsort((f_s, -m_s, r_s))
+        first = np.ones(order.size, bool)
+        first[1:] = r_s[order][1:] != r_s[order][:-1]
+        pick = order[first]
+        m.peak_index = f_s[pick].copy()
+        m.peak_value = full.dense[sel][pick].copy()
+        cs = (full.cand_index >= np.uint64(lo * per_c)) & (full.cand_index < np.uint64(hi * per_c))
+        m.cand_index, m.cand_value = full.cand_index[cs].copy(), full.cand_value[cs].copy()
         out.append(m)
     return out

@@ -125,3 +125,53 @@ def test_c1_range_shards_merge_bit_exactly():
     assert np.array_equal(m.peak_index, a.peak_index) and np.array_equal(m.peak_value, a.peak_value)
     assert np.array_equal(m.cand_index, a.cand_index) and np.array_equal(m.cand_value, a.cand_value)
     assert m.argmax == a.argmax
+
+
+@pytest.mark.parametrize("cfg", [1, 0])
+def test_coarse_shards_merge_bit_exactly(cfg):
+    """The coarse-cell partition (what bench.py runs for N > 1): 3 engines over
+    disjoint coarse-cell slices, every ROI row; their raw peak slots merged on
+    the device (ltci_cuda_merge_peaks) equal the 1-GPU slots bit for bit, the
+    candidate union equals the 1-GPU candidates, the host merge agrees.
+    C1 runs the TMEM FFT path, C0 the tensor path."""
+    import ctypes as C
+
+    import torch
+    from paper_2403_06788_b200 import _lib
+    from paper_2403_06788_b200.parallel import merge_coarse_maps, shard_coarse
+    w = config(cfg)
+    x = scene.to_complex64_roundtrip(w.cube())
+    gamma = detection_threshold(w.params, w.sigma2, 1e-6)
+    opt = DetectorOptions(retain_threshold=gamma)
+    full = Engine(w.params, w.space, opt=opt)
+    full.run_host(x)
+    a = full.result()
+    ptr, n = full.peaks_device()
+    ref_slots = torch.empty((n, 4), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    from bench import _CAI  # __cuda_array_interface__ view of a device pointer
+    ref_slots.copy_(torch.as_tensor(_CAI(ptr, (n, 4), "<i4"), device="cuda"))
+    cells = int(np.prod([g.count for g in w.space.coarse]))
+    world = 3
+    slots = torch.empty((world, n, 4), dtype=torch.int32, device="cuda")
+    maps = []
+    for rank in range(world):
+        lo, hi = shard_coarse(cells, world, rank)
+        e = Engine(w.params, w.space, opt=opt, coarse_begin=lo, coarse_end=hi)
+        e.run_host(x)
+        maps.append(e.result())
+        p2, n2 = e.peaks_device()
+        assert n2 == n
+        slots[rank].copy_(torch.as_tensor(_CAI(p2, (n, 4), "<i4"), device="cuda"))
+        torch.cuda.synchronize()
+        e.close()
+    merged = torch.empty((n, 4), dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    _lib.raise_for(lib.ltci_cuda_merge_peaks(C.c_void_p(slots.data_ptr()), world, n, C.c_void_p(merged.data_ptr()),
+                                             None), lib)
+    torch.cuda.synchronize()
+    assert torch.equal(merged, ref_slots)
+    m = merge_coarse_maps(maps, a.counters)
+    assert np.array_equal(m.cand_index, a.cand_index) and np.array_equal(m.cand_value, a.cand_value)
+    assert np.array_equal(m.peak_index, a.peak_index) and m.argmax == a.argmax
+    full.close()

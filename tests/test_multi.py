@@ -48,6 +48,41 @@ def test_host_merge_reproduces_full_map():
         assert m.argmax == full.argmax and m.argmax_value == full.argmax_value
 
 
+def _small_dense():
+    p = RadarParams.create(3e9, 20e6, 20e6, 1000.0, 64, 128)
+    s = baseline_space(p, [(-150.0, 150.0), (-20.0, 20.0)])
+    x = scene.to_complex64_roundtrip(
+        scene.add_noise(scene.synthesize_cube(p, [(0.2, [40 * p.delta_R(), 61.0, 3.0])]), 1.0 / p.K, 7))
+    full = O.port_ds(x, p, s, DetectorOptions(retain_threshold=2.0, keep_dense=True))
+    C = int(np.prod([g.count for g in s.coarse]))
+    return p, s, full, C
+
+
+def test_shard_coarse_cover_exactly():
+    for C in (8, 83, 332, 3960):
+        for world in (1, 2, 3, 8):
+            sl = [parallel.shard_coarse(C, world, r) for r in range(world)]
+            assert sl[0][0] == 0 and sl[-1][1] == C
+            assert all(a[1] == b[0] for a, b in zip(sl[:-1], sl[1:]))
+    with pytest.raises(ValueError):
+        parallel.shard_coarse(3, 4, 0)
+
+
+def test_host_coarse_merge_reproduces_full_map():
+    """Coarse-cell partition: per-row max across ranks + concatenated candidates
+    reproduce the single-rank map (the oracle's, FP64)."""
+    p, s, full, C = _small_dense()
+    assert np.array_equal(full.peak_index, parallel.split_map_by_coarse(full, C, 1)[0].peak_index)
+    for world in (2, 3, 4):  # C = 4 coarse cells here
+        parts = parallel.split_map_by_coarse(full, C, world)
+        m = parallel.merge_coarse_maps(parts, full.counters)
+        assert np.array_equal(m.peak_index, full.peak_index)
+        assert np.array_equal(m.peak_value, full.peak_value)
+        assert np.array_equal(m.cand_index, full.cand_index)
+        assert np.array_equal(m.cand_value, full.cand_value)
+        assert m.argmax == full.argmax and m.argmax_value == full.argmax_value
+
+
 def _free_port():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
@@ -72,6 +107,39 @@ def _worker(rank, world, port, q):
             q.put(ok)
     finally:
         dist.destroy_process_group()
+
+
+def _worker_coarse(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p, s, full, C = _small_dense()
+        local = parallel.split_map_by_coarse(full, C, world)[rank]
+        merged = parallel.gather_coarse_map(local)
+        if rank == 0:
+            ok = (np.array_equal(merged.peak_index, full.peak_index)
+                  and np.array_equal(merged.peak_value, full.peak_value)
+                  and np.array_equal(merged.cand_index, full.cand_index)
+                  and np.array_equal(merged.cand_value, full.cand_value)
+                  and merged.argmax == full.argmax)
+            q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_coarse_gather_matches_single_rank(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_coarse, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=180)
+        assert pr.exitcode == 0
+    assert q.get(timeout=10) is True
 
 
 @pytest.mark.parametrize("world", [2, 3])
