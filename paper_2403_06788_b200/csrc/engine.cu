@@ -593,6 +593,11 @@ void engine_init(ltci_engine* e) {
     if (pl.variant == LTCI_VARIANT_KTMFP) e->cube_kt.ensure(static_cast<size_t>(pl.rp.K) * M);
 }
 
+__global__ void init_slots_kernel(PeakSlot* __restrict__ slots, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        slots[i] = PeakSlot{0.f, 0.f, ~0ull};
+}
+
 void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
     const Plan& pl = e->pl;
     DeviceGuard dg(e->device);
@@ -608,12 +613,9 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
     std::pair<int, int> kt_ev{-1, -1};
 
     CK(cudaMemsetAsync(e->cand_count.p, 0, sizeof(unsigned long long), st));
-    {
-        // slots: re = im = 0, idx = ~0
-        std::vector<PeakSlot> init(pl.R_slice, PeakSlot{0.f, 0.f, ~0ull});
-        CK(cudaMemcpyAsync(e->slots.p, init.data(), init.size() * sizeof(PeakSlot), cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));  // init lives on the host stack
-    }
+    // slots: re = im = 0, idx = ~0 (on the stream: run_device never blocks the host)
+    init_slots_kernel<<<std::max(1, std::min(148, (pl.R_slice + 255) / 256)), 256, 0, st>>>(e->slots.p, pl.R_slice);
+    CK(cudaGetLastError());
     if (pl.keep_dense) CK(cudaMemsetAsync(e->dense.p, 0, e->dense.n * sizeof(float2), st));
 
     const float2* input = d_cube;

@@ -332,20 +332,41 @@ extern "C" int ltci_cuda_run_pd(const ltci_scenario* scp, ltci_pd_point* out) {
         opt.fine_path = LTCI_FINE_AUTO;
         opt.device = sc.device;
 
-        // one engine per dual-scale detector, reused by every trial
-        std::vector<std::unique_ptr<ltci_engine, EngineFree>> eng(sc.n_detectors);
-        for (int d = 0; d < sc.n_detectors; ++d) {
-            if (sc.detectors[d] == LTCI_FD_GRFT) continue;
-            ltci_engine* e = nullptr;
-            const bool kt = sc.detectors[d] == LTCI_DS_KT_MFP;
-            pd_rc(ltci_engine_create(&sc.radar, &dual, kt ? &amb : nullptr, kt ? LTCI_VARIANT_KTMFP : LTCI_VARIANT_GRFT,
-                                     &opt, 0, -1, &e));
-            eng[d].reset(e);
+        // kLanes (engine set, stream, noisy buffer) triples: trial t runs on lane
+        // t % kLanes, so while the host assembles one trial's candidates and runs
+        // the success test, the next trials are already queued on the device.
+        // One engine per dual-scale detector and lane, reused by every trial.
+        constexpr int kLanes = 3;
+        struct Lane {
+            std::vector<std::unique_ptr<ltci_engine, EngineFree>> eng;
+            cudaStream_t st = nullptr;
+            int trial = -1;  // trial in flight on this lane
+        };
+        std::vector<Lane> lanes(kLanes);
+        for (auto& ln : lanes) {
+            PD_CK(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
+            ln.eng.resize(sc.n_detectors);
+            for (int d = 0; d < sc.n_detectors; ++d) {
+                if (sc.detectors[d] == LTCI_FD_GRFT) continue;
+                ltci_engine* e = nullptr;
+                const bool kt = sc.detectors[d] == LTCI_DS_KT_MFP;
+                pd_rc(ltci_engine_create(&sc.radar, &dual, kt ? &amb : nullptr,
+                                         kt ? LTCI_VARIANT_KTMFP : LTCI_VARIANT_GRFT, &opt, 0, -1, &e));
+                ln.eng[d].reset(e);
+            }
         }
+        struct StreamFree {
+            std::vector<Lane>* l;
+            ~StreamFree() {
+                for (auto& ln : *l)
+                    if (ln.st) cudaStreamDestroy(ln.st);
+            }
+        } stream_free{&lanes};
 
         const size_t n = static_cast<size_t>(sc.radar.K) * sc.radar.M;
         Dev<double2> clean(n);
-        Dev<float2> noisy(n);
+        std::vector<std::unique_ptr<Dev<float2>>> noisy;
+        for (int l = 0; l < kLanes; ++l) noisy.emplace_back(new Dev<float2>(n));
         cudaStream_t st = nullptr;
         const ltci_target& truth = sc.targets[0];
         for (int pt = 0; pt < sc.n_snr; ++pt) {
@@ -358,19 +379,17 @@ extern "C" int ltci_cuda_run_pd(const ltci_scenario* scp, ltci_pd_point* out) {
             }
             synth_device(sc.radar, sc.n_targets, scaled.data(), clean.p, st);
             std::vector<int> wins(sc.n_detectors, 0);
-            for (int trial = 0; trial < sc.trials; ++trial) {
-                const uint64_t seed =
-                    derive_seed(sc.seed, static_cast<uint64_t>(pt) * static_cast<uint64_t>(sc.trials) + trial);
-                ltcib::noise_kernel<<<grid_for(n), 256, 0, st>>>(clean.p, n, sc.sigma2, seed, nullptr, noisy.p);
-                PD_CK(cudaGetLastError());
+            // FD-GRFT runs synchronously on the legacy stream; it waits for the lane's noise kernel
+            auto collect = [&](int l) {
+                Lane& ln = lanes[l];
                 for (int d = 0; d < sc.n_detectors; ++d) {
                     std::unique_ptr<ltci_detection_map, MapFree> map;
                     if (sc.detectors[d] == LTCI_FD_GRFT) {
-                        map.reset(ltcib_fd_grft_device(noisy.p, sc.radar, single, &opt));
+                        PD_CK(cudaStreamSynchronize(ln.st));
+                        map.reset(ltcib_fd_grft_device(noisy[l]->p, sc.radar, single, &opt));
                     } else {
-                        pd_rc(ltci_engine_run_device(eng[d].get(), noisy.p, st));
                         ltci_detection_map* m = nullptr;
-                        pd_rc(ltci_engine_result(eng[d].get(), st, &m));
+                        pd_rc(ltci_engine_result(ln.eng[d].get(), ln.st, &m));
                         map.reset(m);
                     }
                     const bool kt = sc.detectors[d] == LTCI_DS_KT_MFP;
@@ -379,6 +398,24 @@ extern "C" int ltci_cuda_run_pd(const ltci_scenario* scp, ltci_pd_point* out) {
                                         : ltcib_detection_success(map.get(), &dual, nullptr, kt ? &amb : nullptr, truth);
                     wins[d] += ok ? 1 : 0;
                 }
+                ln.trial = -1;
+            };
+            for (int trial = 0; trial < sc.trials; ++trial) {
+                const int l = trial % kLanes;
+                if (lanes[l].trial >= 0) collect(l);
+                const uint64_t seed =
+                    derive_seed(sc.seed, static_cast<uint64_t>(pt) * static_cast<uint64_t>(sc.trials) + trial);
+                ltcib::noise_kernel<<<grid_for(n), 256, 0, lanes[l].st>>>(clean.p, n, sc.sigma2, seed, nullptr,
+                                                                          noisy[l]->p);
+                PD_CK(cudaGetLastError());
+                for (int d = 0; d < sc.n_detectors; ++d)
+                    if (sc.detectors[d] != LTCI_FD_GRFT)
+                        pd_rc(ltci_engine_run_device(lanes[l].eng[d].get(), noisy[l]->p, lanes[l].st));
+                lanes[l].trial = trial;
+            }
+            for (int k = 0; k < kLanes; ++k) {
+                const int l = (sc.trials + k) % kLanes;  // oldest first
+                if (lanes[l].trial >= 0) collect(l);
             }
             for (int d = 0; d < sc.n_detectors; ++d) {
                 ltci_pd_point& o = out[d * sc.n_snr + pt];
