@@ -168,8 +168,10 @@ def cpu_reference_rate(w, seconds_target: float, threads: int):
     # (coarse cell, ROI row) at any row count (the per-cell mgift is < 1 % of it),
     # so large configs keep every coarse/fine cell of the slice but fewer rows
     per_row = sl.integrations() / sl.space.roi.count()
-    rows = int(max(1, min(sl.space.roi.count(), seconds_target * 4e9 * threads / per_row)))
-    if rows < 4 and w.variant == 0 and g0.count >= threads:
+    # at least 4 rows: the reference builds each (coarse, fine) DFM filter once per
+    # row set, so a 1-row sample would mostly time filter construction
+    rows = int(max(min(4, sl.space.roi.count()), min(sl.space.roi.count(), seconds_target * 4e9 * threads / per_row)))
+    if rows <= 4 and w.variant == 0 and g0.count >= threads:
         # huge per-row work (C2): exactly one coarse cell per thread, and enough rows
         # that the reference's per-(coarse, fine) DFM filter build stays amortised
         sl = configs.sliced(w, threads, 1)
