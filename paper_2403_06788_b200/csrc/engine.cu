@@ -423,25 +423,26 @@ void launch_tc_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& 
     CK(cudaGetLastError());
 }
 
-template <bool DENSE>
+template <int Q, int G, bool DENSE>
 void launch_fine_tm(const FineArgs& a, cudaStream_t st) {
-    const size_t smem = fine_tm_smem_floats2() * sizeof(float2);
-    auto kern = fine_fft_tm_kernel<DENSE>;
+    const size_t smem = fine_tm_smem_floats2<Q, G>() * sizeof(float2);
+    auto kern = fine_fft_tm_kernel<Q, G, DENSE>;
     static bool attr_done = false;
     if (!attr_done) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr_done = true;
     }
-    const int blocks = (a.rows + kFineTmThreads / 32 - 1) / (kFineTmThreads / 32);
+    constexpr int rows_per_block = (kFineTmThreads / 32) * (32 / G);
+    const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
     kern<<<blocks, kFineTmThreads, smem, st>>>(a);
     CK(cudaGetLastError());
 }
 
 template <int Q, int G, bool DENSE>
 void launch_fine_qg(const FineArgs& a, cudaStream_t st) {
-    if constexpr (Q == 32 && G == 32) {
-        if (!std::getenv("LTCI_FINE_TM_OFF")) {  // TMEM-resident row variant (M = 1024)
-            launch_fine_tm<DENSE>(a, st);
+    if constexpr (Q == 32 && (G == 32 || G == 16 || G == 8)) {
+        if (!std::getenv("LTCI_FINE_TM_OFF")) {  // TMEM-resident row variant (M = 1024, 512, 256)
+            launch_fine_tm<Q, G, DENSE>(a, st);
             return;
         }
     }

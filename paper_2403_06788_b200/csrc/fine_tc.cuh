@@ -830,14 +830,12 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
         return true;
     }
     if (fine_path == 1) return false;  // explicit CUDA-core FFT path
-    // AUTO (by measurement): M = 1024 runs the CUDA-core FFT
-    // path with the TMEM-resident row (C1: 226 ms vs 250 ms tensor 3-term;
-    // C3 KT, D = M: 39 ms, the dense form is ~8x the work); M > 1024 has only
-    // the tensor path; otherwise the 3-term (FP32-class) tensor path for
-    // Doppler-windowed DS-GRFT (C0, M = 256, D = 151: 0.68 vs 1.25 ms; C4,
-    // M = 512: 12.3 vs 16.7 ms/CPI) and the FFT path for small M or a wide
-    // Doppler window.
-    if (M == 1024) return false;
+    // AUTO (by measurement): M = 256..1024 runs the CUDA-core
+    // FFT path with TMEM-resident rows (C1: 222 vs 246 ms tensor 3-term; C4:
+    // 8.7 vs 12.3 ms per CPI; C0: 0.56 vs 0.69 ms; C3 KT, D = M: the dense
+    // form is ~8x the work); M > 1024 has only the tensor path; below 256 the
+    // 3-term (FP32-class) tensor path for a narrow Doppler window, else FFT.
+    if (M >= 256 && M <= 1024) return false;
     if (keep_dense) return M > 1024;
     return M > 1024 || (M >= 64 && (D <= 160 || 2 * D <= M));
 }

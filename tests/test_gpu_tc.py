@@ -96,7 +96,7 @@ def test_fine_path_selection_is_honoured():
     from paper_2403_06788_b200.detectors import Engine
     w = config(0)
     for req, want in ((A.FINE_FFT_CUDA_CORE, A.FINE_FFT_CUDA_CORE), (A.FINE_TC_DENSE, A.FINE_TC_DENSE),
-                      (A.FINE_TC_FAST, A.FINE_TC_FAST), (A.FINE_AUTO, A.FINE_TC_DENSE)):
+                      (A.FINE_TC_FAST, A.FINE_TC_FAST), (A.FINE_AUTO, A.FINE_FFT_CUDA_CORE)):
         e = Engine(w.params, w.space, opt=DetectorOptions(fine_path=req))
         assert e.fine_path()[0] == want
         e.close()
@@ -107,4 +107,8 @@ def test_fine_path_selection_is_honoured():
     w1 = config(1)
     e = Engine(w1.params, w1.space, opt=DetectorOptions())
     assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE  # M = 1024: TMEM-resident FFT path
+    e.close()
+    w2 = config(2)
+    e = Engine(w2.params, w2.space, opt=DetectorOptions())
+    assert e.fine_path()[0] == A.FINE_TC_DENSE  # M = 2048: tensor path only
     e.close()
