@@ -1,0 +1,72 @@
+"""The TMEM-resident FFT fine kernel (fine_fft_tm_kernel<32, G>, M = 256, 512,
+1024) against the FP64 C restatement: orders 1, 2 and 3 (the order-3 space has
+two fine axes, so the kernel's outer/inner fine loop and its per-outer chirp
+seeds run), DS-GRFT and DS-KT-MFP, dense maps (the DENSE instantiation),
+candidates and per-range-cell peaks."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2403_06788_b200 import _cabi as A
+from paper_2403_06788_b200 import scene
+from paper_2403_06788_b200.detectors import Engine
+from paper_2403_06788_b200.model import (Bounds, DetectorOptions, RadarParams, RangeRoi, build_ambiguity,
+                                         build_dual_scale)
+
+from helpers import TOL, check_candidates, check_peaks, max_rel
+
+pytestmark = pytest.mark.gpu
+
+CASES = [  # (M, P, bounds, alpha)
+    (256, 1, [(-40.0, 40.0)], [1.0]),
+    (256, 3, [(-30.0, 30.0), (-6.0, 6.0), (-3.0, 3.0)], [0.4, 0.3, 0.3]),
+    (512, 2, [(-30.0, 30.0), (-6.0, 6.0)], [0.5, 0.5]),
+    (512, 3, [(-20.0, 20.0), (-3.0, 3.0), (-0.8, 0.8)], [0.4, 0.3, 0.3]),
+    (1024, 1, [(-20.0, 20.0)], [1.0]),
+    (1024, 3, [(-10.0, 10.0), (-1.0, 1.0), (-0.3, 0.3)], [0.4, 0.3, 0.3]),
+]
+
+
+def _setup(M, P, bounds, alpha, K=64):
+    p = RadarParams.create(8 * 100e6, 100e6, 50e6, 2000.0, M, K)  # fc/fs = 8: several fine cells per axis
+    s = build_dual_scale(p, P, [Bounds(*b) for b in bounds], alpha, RangeRoi(2, K - 3))
+    coeffs = [20 * p.delta_R()] + [0.3 * b[1] for b in bounds]
+    x = scene.to_complex64_roundtrip(
+        scene.add_noise(scene.synthesize_cube(p, [(0.05, coeffs)]), 1.0 / K, M + P))
+    return p, s, x
+
+
+@pytest.mark.parametrize("M,P,bounds,alpha", CASES)
+def test_tm_fft_dense_vs_oracle(M, P, bounds, alpha):
+    p, s, x = _setup(M, P, bounds, alpha)
+    retain = 0.3 * float(M)
+    opt = DetectorOptions(retain_threshold=retain, keep_dense=True)
+    e = Engine(p, s, opt=opt)
+    assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE
+    e.run_host(x)
+    gm = e.result()
+    e.close()
+    rm = O.port_ds(x, p, s, opt)
+    assert gm.counters == rm.counters
+    assert max_rel(gm.dense, rm.dense) <= TOL
+    assert np.abs(gm.dense - rm.dense).max() / np.abs(rm.dense).max() <= TOL
+    check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, retain)
+    check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
+
+
+@pytest.mark.parametrize("M", [256, 512, 1024])
+def test_tm_fft_kt_vs_oracle(M):
+    p, s, x = _setup(M, 2, [(-30.0, 30.0), (-6.0, 6.0)], [0.5, 0.5])
+    amb = build_ambiguity(p, Bounds(-1.6 * p.Va(), 1.6 * p.Va()))
+    opt = DetectorOptions(retain_threshold=0.3 * float(M), keep_dense=True)
+    e = Engine(p, s, 1, amb, opt)
+    assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE
+    e.run_host(x)
+    gk = e.result()
+    e.close()
+    rk = O.port_ds(x, p, s, opt, 1, amb)
+    assert gk.counters == rk.counters
+    assert max_rel(gk.dense, rk.dense) <= TOL
+    check_peaks(gk.peak_index, gk.peak_value, rk.peak_index, rk.peak_value, value_at=lambda i: rk.dense[i])
