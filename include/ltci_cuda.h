@@ -43,7 +43,7 @@ extern "C" {
 #endif
 
 #define LTCI_MAX_ORDER 4
-#define LTCI_MAX_AXES 8
+#define LTCI_MAX_AXES 12  /* DS-GRFT has 2P + 1 axes: 9 at P = 4 */
 
 /* status codes: the C++ shim rethrows the matching exception type */
 enum {

@@ -8,7 +8,7 @@ from __future__ import annotations
 import ctypes as C
 
 MAX_ORDER = 4
-MAX_AXES = 8
+MAX_AXES = 12
 
 OK, INVALID_ARGUMENT, CONDITION_VIOLATED, RUNTIME_ERROR, BAD_ALLOC, NO_DEVICE, IO_ERROR = range(7)
 FD_GRFT, TD_GRFT, KT_MFP, DS_GRFT, DS_KT_MFP = range(5)

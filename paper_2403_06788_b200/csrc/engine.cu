@@ -901,6 +901,7 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
     if (!out) throw std::bad_alloc();
     try {
         out->kind = pl.variant == LTCI_VARIANT_GRFT ? LTCI_DS_GRFT : LTCI_DS_KT_MFP;
+        if (pl.axes.size() > LTCI_MAX_AXES) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: too many map axes");
         out->n_axes = static_cast<int32_t>(pl.axes.size());
         for (size_t i = 0; i < pl.axes.size(); ++i) out->axes[i] = pl.axes[i];
         for (int i = 0; i < 4; ++i) out->counters[i] = pl.counters[i];

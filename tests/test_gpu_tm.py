@@ -70,3 +70,25 @@ def test_tm_fft_kt_vs_oracle(M):
     assert gk.counters == rk.counters
     assert max_rel(gk.dense, rk.dense) <= TOL
     check_peaks(gk.peak_index, gk.peak_value, rk.peak_index, rk.peak_value, value_at=lambda i: rk.dense[i])
+
+
+@pytest.mark.parametrize("path", [A.FINE_FFT_CUDA_CORE, A.FINE_TC_DENSE])
+def test_order_four_both_paths_vs_oracle(path):
+    """P = 4 (three fine axes: the outer fine loop spans two of them) on the
+    TMEM FFT path and the tensor path."""
+    M, K = 256, 64
+    p = RadarParams.create(8 * 100e6, 100e6, 50e6, 2000.0, M, K)
+    s = build_dual_scale(p, 4, [Bounds(-20.0, 20.0), Bounds(-4.0, 4.0), Bounds(-1.0, 1.0), Bounds(-0.3, 0.3)],
+                         [0.4, 0.2, 0.2, 0.2], RangeRoi(4, K - 5))
+    x = scene.to_complex64_roundtrip(scene.add_noise(
+        scene.synthesize_cube(p, [(0.05, [24 * p.delta_R(), 5.0, 1.0, 0.2, 0.05])]), 1.0 / K, 44))
+    opt = DetectorOptions(retain_threshold=0.3 * M, keep_dense=True, fine_path=path)
+    e = Engine(p, s, opt=opt)
+    assert e.fine_path()[0] == path
+    e.run_host(x)
+    gm = e.result()
+    e.close()
+    rm = O.port_ds(x, p, s, opt)
+    assert gm.counters == rm.counters
+    assert max_rel(gm.dense, rm.dense) <= TOL
+    check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
