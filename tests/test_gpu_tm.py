@@ -92,3 +92,25 @@ def test_order_four_both_paths_vs_oracle(path):
     assert gm.counters == rm.counters
     assert max_rel(gm.dense, rm.dense) <= TOL
     check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
+
+
+@pytest.mark.parametrize("path", [A.FINE_FFT_CUDA_CORE, A.FINE_TC_DENSE])
+@pytest.mark.parametrize("roi", [(0, 0), (63, 63), (60, 63), (0, 63)])
+def test_roi_edges_both_paths(path, roi):
+    """One-row and edge ROIs (tile tails of the tensor path, single-row CTAs of
+    the FFT path) against the oracle, with fine grids of several cells."""
+    M, K = 512, 64
+    p = RadarParams.create(8 * 100e6, 100e6, 50e6, 2000.0, M, K)
+    s = build_dual_scale(p, 2, [Bounds(-30.0, 30.0), Bounds(-6.0, 6.0)], [0.5, 0.5], RangeRoi(*roi))
+    x = scene.to_complex64_roundtrip(scene.add_noise(
+        scene.synthesize_cube(p, [(0.05, [(roi[0] + 0) * p.delta_R(), 5.0, 1.0])]), 1.0 / K, 7 + roi[0]))
+    opt = DetectorOptions(retain_threshold=0.2 * M, keep_dense=True, fine_path=path)
+    e = Engine(p, s, opt=opt)
+    e.run_host(x)
+    gm = e.result()
+    e.close()
+    rm = O.port_ds(x, p, s, opt)
+    assert gm.counters == rm.counters and gm.peak_index.size == roi[1] - roi[0] + 1
+    assert max_rel(gm.dense, rm.dense) <= TOL
+    check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, 0.2 * M)
+    check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
