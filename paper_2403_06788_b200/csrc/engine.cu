@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <set>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -312,17 +314,26 @@ void radix_plan(int K, int* radix, int* npass) {
     *npass = n;
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: set it
+// once per (kernel, device), so one process may drive engines on several GPUs
+void ensure_smem_attr(const void* kern, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({kern, dev})) return;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({kern, dev});
+}
+
 int coarse_pg(int K, int M) { return coarse_pg_for(K, M); }
 
 template <int K, int OUT16>
 void launch_coarse_k(const CoarseArgs& a, cudaStream_t st) {
     auto kern = coarse_rm_kernel<K, OUT16>;
     const size_t smem = coarse_smem_bytes(K, a.M);
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr_done = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), 160 * 1024);
     dim3 grid(a.M / coarse_pg_for(K, a.M), a.c_count);
     kern<<<grid, kCoarseThreads, smem, st>>>(a);
     CK(cudaGetLastError());
@@ -387,7 +398,7 @@ template <int TERMS>
 void launch_tc2_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& lo, cudaStream_t st) {
     auto kern = fine_tc2_kernel<TERMS>;
     const size_t smem = tc2_smem_bytes(TERMS);
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     const long long Q = static_cast<long long>(a.f.F) * a.f.D;
     const long long tiles = ((Q + TC_QT - 1) / TC_QT) * ((a.f.rows + 2 * TC2_BM - 1) / (2 * TC2_BM));
     int dev = 0, sms = 148;
@@ -412,7 +423,7 @@ void launch_tc_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& 
     auto kern = fine_tc_kernel<TERMS>;
     const size_t smem = tc_smem_bytes(TERMS, a.M);
     if (smem > 227 * 1024) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: tcgen05 tiles exceed shared memory");
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     const long long Q = static_cast<long long>(a.f.F) * a.f.D;
     const long long tiles = ((Q + TC_QT - 1) / TC_QT) * ((a.f.rows + TC_BM - 1) / TC_BM);
     int dev = 0, sms = 148;
@@ -427,11 +438,7 @@ template <int Q, int G, bool DENSE>
 void launch_fine_tm(const FineArgs& a, cudaStream_t st) {
     const size_t smem = fine_tm_smem_floats2<Q, G>() * sizeof(float2);
     auto kern = fine_fft_tm_kernel<Q, G, DENSE>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr_done = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     constexpr int rows_per_block = (kFineTmThreads / 32) * (32 / G);
     const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
     kern<<<blocks, kFineTmThreads, smem, st>>>(a);
@@ -449,11 +456,7 @@ void launch_fine_qg(const FineArgs& a, cudaStream_t st) {
     constexpr int rows_per_block = (kFineThreads / 32) * (32 / G);
     const size_t smem = fine_smem_floats2<Q, G>() * sizeof(float2);
     auto kern = fine_fft_kernel<Q, G, DENSE>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_done = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), 200 * 1024);
     const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
     kern<<<blocks, kFineThreads, smem, st>>>(a);
     CK(cudaGetLastError());
@@ -1011,11 +1014,7 @@ void fd_launch_batch(const FdArgs& a, cudaStream_t st) {
     auto sc = fd_fft_scan_kernel<K>;
     constexpr int PG = kCoarseSamples / K;
     const size_t smem_sc = static_cast<size_t>(PG) * coarse_kp(K) * sizeof(float2);
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        CK(cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_done = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(sc), 200 * 1024);
     mf<<<static_cast<unsigned>((a.c_count + fd_cells(K) - 1) / fd_cells(K)), fd_threads(K), smem_mf, st>>>(a);
     CK(cudaGetLastError());
     sc<<<static_cast<unsigned>((a.c_count + PG - 1) / PG), kCoarseThreads, smem_sc, st>>>(a);
