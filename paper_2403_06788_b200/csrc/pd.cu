@@ -315,7 +315,14 @@ extern "C" int ltci_cuda_run_pd(const ltci_scenario* scp, ltci_pd_point* out) {
             if (sc.detectors[d] != LTCI_FD_GRFT && sc.detectors[d] != LTCI_DS_GRFT &&
                 sc.detectors[d] != LTCI_DS_KT_MFP)
                 throw std::invalid_argument("run_pd: detector not built on the GPU (fd_grft, ds_grft, ds_kt_mfp)");
-        cudaSetDevice(sc.device);
+        struct DeviceRestore {  // the caller's current device is left as it was
+            int prev = 0;
+            explicit DeviceRestore(int dev) {
+                cudaGetDevice(&prev);
+                if (dev != prev) PD_CK(cudaSetDevice(dev));
+            }
+            ~DeviceRestore() { cudaSetDevice(prev); }
+        } device_restore(sc.device);
 
         // build_spaces (bench.cpp:13-21)
         const ltci_single_space single = build_single(sc, 0, sc.radar.K - 1);
