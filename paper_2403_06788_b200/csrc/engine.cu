@@ -1010,19 +1010,25 @@ namespace {
 template <int K>
 void fd_launch_batch(const FdArgs& a, cudaStream_t st) {
     auto mf = fd_mf_kernel<K>;
-    const size_t smem_mf = 0;
-    auto sc = fd_fft_scan_kernel<K>;
-    constexpr int PG = kCoarseSamples / K;
-    const size_t smem_sc = static_cast<size_t>(PG) * coarse_kp(K) * sizeof(float2);
-    ensure_smem_attr(reinterpret_cast<const void*>(sc), 200 * 1024);
-    mf<<<static_cast<unsigned>((a.c_count + fd_cells(K) - 1) / fd_cells(K)), fd_threads(K), smem_mf, st>>>(a);
+    mf<<<static_cast<unsigned>((a.c_count + fd_cells(K) - 1) / fd_cells(K)), fd_threads(K), 0, st>>>(a);
     CK(cudaGetLastError());
-    sc<<<static_cast<unsigned>((a.c_count + PG - 1) / PG), kCoarseThreads, smem_sc, st>>>(a);
+    if constexpr (K < 16) {
+        fd_small_scan_kernel<K><<<static_cast<unsigned>((a.c_count + 255) / 256), 256, 0, st>>>(a);
+    } else {
+        auto sc = fd_fft_scan_kernel<K>;
+        constexpr int PG = kCoarseSamples / K;
+        const size_t smem_sc = static_cast<size_t>(PG) * coarse_kp(K) * sizeof(float2);
+        ensure_smem_attr(reinterpret_cast<const void*>(sc), 200 * 1024);
+        sc<<<static_cast<unsigned>((a.c_count + PG - 1) / PG), kCoarseThreads, smem_sc, st>>>(a);
+    }
     CK(cudaGetLastError());
 }
 
 void fd_launch(const FdArgs& a, cudaStream_t st) {
     switch (a.K) {
+        case 2: fd_launch_batch<2>(a, st); break;
+        case 4: fd_launch_batch<4>(a, st); break;
+        case 8: fd_launch_batch<8>(a, st); break;
         case 16: fd_launch_batch<16>(a, st); break;
         case 32: fd_launch_batch<32>(a, st); break;
         case 64: fd_launch_batch<64>(a, st); break;
@@ -1041,7 +1047,7 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
                                 const ltci_single_space& s, const ltci_options* opt) {
     validate_radar(rp);
     check_same_params(rp, s.radar);
-    if (rp.K < 16 || rp.K > 8192) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be in [16, 8192]");
+    if (rp.K < 2 || rp.K > 8192) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be in [2, 8192]");
     if (rp.M > 1 << 20) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: fd_grft supports M <= 2^20");
     const int P = s.order;
     if (P < 1 || P > LTCI_MAX_ORDER) fail(LTCI_INVALID_ARGUMENT, "fd_grft: order must be in [1, 4]");

@@ -282,4 +282,58 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) fd_fft_scan_kernel(FdArgs a
     }
 }
 
+// K < 16 (the reference accepts any power of two): one cell per thread, the
+// K-point dft_plus in registers, then the same ROI scan and argmax publish.
+template <int K>
+__global__ void __launch_bounds__(256) fd_small_scan_kernel(FdArgs a) {
+    static_assert(K >= 2 && K < 16, "small-K transform");
+    const unsigned long long cell = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    float bm = -1.0f;
+    unsigned long long bidx = ~0ull;
+    float2 bv = make_float2(0.f, 0.f);
+    if (cell < a.c_count) {
+        float2 v[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) v[r] = a.acc[cell * K + r];
+        dft_reg<K>(v);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int r = k - a.roi_first;
+            if (r < 0 || r >= a.R) continue;
+            const float m2 = mag2f(v[k].x, v[k].y);
+            const unsigned long long flat = (a.c_begin + cell) * static_cast<unsigned long long>(a.R) + r;
+            if (a.dense) a.dense[flat] = v[k];
+            if (m2 > a.retain2) {
+                const unsigned long long at = atomicAdd(a.cand_count, 1ull);
+                if (at < a.cand_cap) {
+                    CandRec rec;
+                    rec.idx = flat;
+                    rec.re = v[k].x;
+                    rec.im = v[k].y;
+                    a.cand[at] = rec;
+                }
+            }
+            if (m2 > bm || (m2 == bm && flat < bidx)) {
+                bm = m2;
+                bidx = flat;
+                bv = v[k];
+            }
+        }
+    }
+    // warp argmax, one publish per warp
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, bm, off);
+        const unsigned long long oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+        const float ore = __shfl_xor_sync(0xffffffffu, bv.x, off);
+        const float oim = __shfl_xor_sync(0xffffffffu, bv.y, off);
+        if (om > bm || (om == bm && oi < bidx)) {
+            bm = om;
+            bidx = oi;
+            bv = make_float2(ore, oim);
+        }
+    }
+    if ((threadIdx.x & 31) == 0 && bidx != ~0ull) peak_publish(a.best, bv.x, bv.y, bidx);
+}
+
 }  // namespace ltcib

@@ -139,14 +139,17 @@ def test_fd_grft_vs_reference_live():
 
 @pytest.mark.gpu
 @needs_ref
-@pytest.mark.parametrize("K,M", [(16, 64), (128, 32), (512, 16), (1024, 16), (2048, 8), (4096, 8), (8192, 4)])
+@pytest.mark.parametrize("K,M", [(2, 16), (4, 16), (8, 8), (16, 64), (128, 32), (512, 16), (1024, 16), (2048, 8),
+                                 (4096, 8), (8192, 4)])
 def test_fd_grft_all_sizes_vs_reference(K, M):
     """Dense maps against the reference at every supported K (transform radix
     plans 16 .. 16x16x16x2, rotor chains of 1 .. 32 rows per thread)."""
     from paper_2403_06788_b200 import fd_grft, scene
     p = RadarParams.create(3e9, 20e6, 18e6, 1000.0, M, K)
     x = scene.to_complex64_roundtrip(scene.add_noise(np.zeros((M, K), complex), 1.0, K + M))
-    s = build_single_scale(p, 2, [Bounds(-40.0, 40.0), Bounds(-8000.0, 8000.0)], [0.5, 0.5], RangeRoi(1, K - 2))
+    lo = min(1, K - 1)
+    s = build_single_scale(p, 2, [Bounds(-40.0, 40.0), Bounds(-8000.0, 8000.0)], [0.5, 0.5],
+                           RangeRoi(lo, max(K - 2, lo)))
     s.c[0].count = min(s.c[0].count, 7)
     s.c[1].count = min(s.c[1].count, 3)
     opt = DetectorOptions(retain_threshold=0.0, keep_dense=True)

@@ -2,15 +2,20 @@
 relinked against the B200 drop-in (oracle/Makefile target `dropin`): every
 call to ltci::ds_grft / ltci::ds_kt_mfp inside it runs on the GPU, every
 other function (fd_grft_point, kt_mfp_point, keystone, extract_detections,
-synthesis) is the reference's own.  Criteria exercising the hot path:
-  2 peak law, 3 DS-GRFT factorization (100 random targets),
-  4 DS-KT-MFP factorization (100), 9 full-scale three-target scene.
+synthesis) is the reference's own.  All ten criteria pass; the ones exercising
+the hot path: 2 peak law, 3 DS-GRFT factorization (100 random targets),
+4 DS-KT-MFP factorization (100), 7 operation counters equal the complexity
+model (30 runs), 8 desk-scale detection-probability ordering, 9 full-scale
+three-target scene, 10 complexity crossover.
 acceptance_dropin_fd additionally routes ltci::fd_grft to the GPU (SURVEY.md
-8(f) rank 2): criterion 3 (fd vs ds on 100 targets) and criterion 6 (threshold
-calibration, 100 000 noise-only fd_grft calls in under 60 s).  Criteria 1 and 2
-check fd_grft against literal sums at 1e-9 relative error, i.e. FP64
-definitional equality, outside the FP32 contract of this port (1e-3, BASELINE
-north_star); they run against the reference's fd_grft in acceptance_dropin."""
+8(f) rank 2): criteria 3-6 and 8-10 pass (3: fd vs ds on 100 targets; 6:
+threshold calibration, 100 000 noise-only fd_grft calls in under 60 s; 8: the
+FD/DS Pd ordering).  By design three do not: 1 and 2 check fd_grft against
+literal sums at 1e-9 relative error, i.e. FP64 definitional equality, outside
+the FP32 contract of this port (1e-3, BASELINE north_star); 7 asserts that the
+single-scale search is slower than the dual-scale one, which the CPU cost
+model predicts and the GPU no longer shows (both under a millisecond there).
+They run against the reference's fd_grft in acceptance_dropin."""
 from __future__ import annotations
 
 import os
@@ -26,7 +31,7 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not os.path.exists(BIN), reason="drop-in acceptance binary not built")]
 
 
-@pytest.mark.parametrize("criterion", [2, 3, 4, 9])
+@pytest.mark.parametrize("criterion", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
 def test_reference_acceptance_through_dropin(criterion):
     env = dict(os.environ, LTCI_THREADS=str(os.cpu_count() or 1))
     r = subprocess.run([BIN, str(criterion)], capture_output=True, text=True, timeout=900, env=env)
@@ -36,7 +41,7 @@ def test_reference_acceptance_through_dropin(criterion):
 
 
 @pytest.mark.skipif(not os.path.exists(BIN_FD), reason="fd drop-in acceptance binary not built")
-@pytest.mark.parametrize("criterion", [3, 6])
+@pytest.mark.parametrize("criterion", [3, 4, 5, 6, 8, 9, 10])
 def test_reference_acceptance_fd_through_dropin(criterion):
     env = dict(os.environ, LTCI_THREADS=str(os.cpu_count() or 1))
     r = subprocess.run([BIN_FD, str(criterion)], capture_output=True, text=True, timeout=900, env=env)
