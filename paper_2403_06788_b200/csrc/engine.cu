@@ -439,9 +439,9 @@ void launch_fine_tm(const FineArgs& a, cudaStream_t st) {
     const size_t smem = fine_tm_smem_floats2<Q, G>() * sizeof(float2);
     auto kern = fine_fft_tm_kernel<Q, G, DENSE>;
     ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
-    constexpr int rows_per_block = (kFineTmThreads / 32) * (32 / G);
+    constexpr int rows_per_block = fine_tm_warps<Q, G>() * (32 / G);
     const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
-    kern<<<blocks, kFineTmThreads, smem, st>>>(a);
+    kern<<<blocks, fine_tm_warps<Q, G>() * 32, smem, st>>>(a);
     CK(cudaGetLastError());
 }
 
