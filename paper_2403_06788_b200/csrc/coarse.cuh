@@ -40,30 +40,62 @@ struct CoarseArgs {
 };
 
 
-// One CTA = PG pulses x one coarse cell, PG * K = kCoarseSamples (PG = 8 at
-// K = 2048, so an fp16 output row segment is one full 32-byte sector).
-// The K-point transform is an in-place mixed-radix decimation-in-frequency
-// FFT (radices 16, ..., 16, R_last): every butterfly reads and writes its own
-// positions, so a pass needs one barrier and only R values per thread.
-//   pass 1     global loads (all in flight) -> fractional ramp -> DFT16 ->
+// One CTA = PG pulses x one coarse cell, PG * K = coarse_samples(OUT16)
+// (PG = 4 fp32 / 8 fp16 pulses at K = 2048: an output row segment is one full
+// 32-byte sector either way).  The K-point transform is an in-place
+// mixed-radix decimation-in-frequency FFT (radices 16, ..., 16, R_last):
+// every butterfly reads and writes its own positions, so a pass needs one
+// barrier and only R values per thread.
+//   pass 1     global loads (all in flight) -> phase ramp -> DFT16 ->
 //              twiddle -> shared
 //   middle     shared -> DFT16 -> twiddle -> shared (same positions)
-//   last       shared -> preDFM -> DFT_R -> per-pulse rotation -> global
-// The last pass produces, per (pulse p, row group g), the R rows g + G t
-// (G = K / R) directly: the integer part of the pulse's shift becomes a
-// rotation of the output index (an exact register barrel shift after the
-// DFT), so lanes p = 0..PG-1 of a warp write the same row (PG contiguous
-// pulses) and every value depends only on its absolute bin.
-constexpr int kCoarseThreads = 512;
+//   last       shared -> DFT_R -> global
+// The pass-1 ramp carries the whole per-(cell, pulse) phase: the fractional
+// delay and keystone terms, the preDFM factor and the integer part s of the
+// shift as the exact linear phase (k s mod K) / K cycles (reduced in integers,
+// so every FP32 sincos argument stays within 2.5 pi + |b| g^2).  The last pass
+// therefore emits absolute bins: the thread of residue kl owns bins
+// kl + G t, lanes p = 0..PG-1 of a warp write the same row (PG contiguous
+// pulses), and a row's value depends only on its absolute bin (range-cell
+// shards reproduce the 1-GPU map bit for bit).
+constexpr int kCoarseThreads = 512;      // fp16-output (tcgen05 path) CTAs and fd_grft
 constexpr int kCoarseSamples = 16384;
+template <int OUT16>
+__host__ __device__ constexpr int coarse_threads() { return OUT16 ? kCoarseThreads : 256; }
+template <int OUT16>
+__host__ __device__ constexpr int coarse_min_blocks() { return OUT16 ? 1 : 3; }
+__host__ __device__ constexpr int coarse_samples(int out16) { return out16 ? kCoarseSamples : 8192; }
 
-__host__ __device__ constexpr int coarse_pg_for(int K, int M) {
-    return (kCoarseSamples / K) < M ? (kCoarseSamples / K) : M;
+__host__ __device__ constexpr int coarse_pg_for(int K, int M, int out16 = 1) {
+    return (coarse_samples(out16) / K) < M ? (coarse_samples(out16) / K) : M;
 }
 // 8 float2 of padding per 128 (2-way worst case in the middle passes; keeps
 // 8-element runs 16-byte aligned), plus 4 float2 per pulse buffer
 __host__ __device__ constexpr int cpad(int i) { return i + ((i >> 7) << 3); }
 __host__ __device__ constexpr int coarse_kp(int K) { return cpad(K) + 4; }
+
+// Pulse-buffer layouts.  SW = false: the padded layout above.  SW = true
+// (K = 2048, fp32 output; 16 radix-16 blocks of 128 per pulse): no padding;
+// position i is XOR-swizzled in its low 4 bits by g(i >> 7), g(b) = rotr4(b),
+// and pulses are K + 2 apart.  With that every access pattern of the three
+// passes is conflict-free for 64-bit accesses: pass-1 stores (lanes j, one
+// block), middle reads/writes (lanes j < 8 over block pairs b, b + 1:
+// g(b) ^ g(b + 1) = 8), and last-pass reads (lanes = 4 pulses x 4 blocks:
+// {r ^ g(b)} is a coset of {0, 1, 8, 9}, the pulse stride moves it by 2p).
+template <int K, bool SW>
+struct CLayout {
+    static constexpr int kp = SW ? K + 2 : coarse_kp(K);
+    static __device__ __forceinline__ int idx(int i) {
+        if constexpr (SW) {
+            const int b = (i >> 7) & 15;
+            return i ^ (((b & 1) << 3) | (b >> 1));
+        } else {
+            return cpad(i);
+        }
+    }
+};
+template <int K, int OUT16>
+constexpr bool coarse_swizzled() { return K == 2048 && !OUT16; }
 
 // v[r] *= (e^{+j 2 pi num / den})^r, r = 1 .. R-1
 template <int R>
@@ -107,54 +139,35 @@ __device__ __forceinline__ int coarse_digit_rev(int kl) {
     return pos;
 }
 
-template <int K, int R, int OUT16>
+template <int K, int R, int OUT16, int NT, bool SW>
 __device__ __forceinline__ void coarse_last_pass(const CoarseArgs& a, const float2* __restrict__ buf, int PG,
-                                                 int lg_pg, const int* s_shift, const float2* s_pre, float sc,
-                                                 int tid) {
-    constexpr int Kp = coarse_kp(K);
+                                                 int lg_pg, float sc, int tid) {
+    constexpr int Kp = CLayout<K, SW>::kp;
     constexpr int G = K / R;
     constexpr int NREV = R == 1 ? coarse_npass(K) : coarse_npass(K) - 1;  // R == 1: K = 16, one pass
     const int total = PG * G;
     const size_t cbase = static_cast<size_t>(blockIdx.y) * a.R_slice * a.M;
     const int m0 = blockIdx.x * PG;
-    for (int idx = tid; idx < total; idx += kCoarseThreads) {
+    for (int idx = tid; idx < total; idx += NT) {
         const int p = idx & (PG - 1);  // lanes run over pulses first: one row per PG lanes
-        const int g = idx >> lg_pg;
-        const int A = g + a.n_base + s_shift[p];
-        const int kl = A & (G - 1);
-        const int c = (A / G) & (R - 1);
+        const int kl = idx >> lg_pg;   // this thread's bins: kl + G t
         const int pos0 = coarse_digit_rev<K, NREV>(kl);
         const float2* src = buf + p * Kp;
         float2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = src[cpad(pos0 + r)];
-        const float2 pre = make_float2(s_pre[p].x * sc, s_pre[p].y * sc);
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = cmul(v[r], pre);
+        for (int r = 0; r < R; ++r) v[r] = src[CLayout<K, SW>::idx(pos0 + r)];
         dft_reg<R>(v);
-        // output t <- bin kl + G (t + c): an exact barrel rotation of the R outputs
-        // (no arithmetic, so a row's value depends only on its absolute bin and
-        // range-cell shards reproduce the 1-GPU map bit for bit)
-#pragma unroll
-        for (int b = 1; b < R; b <<= 1) {
-            if (c & b) {
-                float2 w[R];
-#pragma unroll
-                for (int t = 0; t < R; ++t) w[t] = v[(t + b) & (R - 1)];
-#pragma unroll
-                for (int t = 0; t < R; ++t) v[t] = w[t];
-            }
-        }
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            const int n = g + G * t;
+            const int n = (kl + G * t - a.n_base) & (K - 1);  // row of bin kl + G t
             if (n < a.R_slice) {
                 const size_t o = cbase + static_cast<size_t>(n) * a.M + m0 + p;
                 if (OUT16) {
                     // x = x_hi + x_lo in fp16 (interleaved re, im along K)
-                    __half2 hi = __floats2half2_rn(v[t].x, v[t].y);
+                    const float2 x = make_float2(v[t].x * sc, v[t].y * sc);
+                    __half2 hi = __floats2half2_rn(x.x, x.y);
                     const float2 hf = __half22float2(hi);
-                    __half2 lo = __floats2half2_rn(v[t].x - hf.x, v[t].y - hf.y);
+                    __half2 lo = __floats2half2_rn(x.x - hf.x, x.y - hf.y);
                     a.Xh[o] = *reinterpret_cast<uint32_t*>(&hi);
                     a.Xl[o] = *reinterpret_cast<uint32_t*>(&lo);
                 } else {
@@ -166,13 +179,13 @@ __device__ __forceinline__ void coarse_last_pass(const CoarseArgs& a, const floa
 }
 
 // middle DIF passes: radix 16 within blocks of length L (K/16 >= L > R_last)
-template <int K, int L>
+template <int K, int L, int NT = kCoarseThreads, bool SW = false>
 __device__ __forceinline__ void coarse_middle_passes(float2* __restrict__ buf, int PG, int tid) {
     if constexpr (L > coarse_last_radix(K)) {
-        constexpr int Kp = coarse_kp(K);
+        constexpr int Kp = CLayout<K, SW>::kp;
         constexpr int S = L / 16;
         constexpr int per = K / 16;  // butterflies per pulse
-        for (int idx = tid; idx < PG * per; idx += kCoarseThreads) {
+        for (int idx = tid; idx < PG * per; idx += NT) {
             const int p = idx / per;
             const int rem = idx - p * per;
             const int blk = rem / S;
@@ -181,35 +194,38 @@ __device__ __forceinline__ void coarse_middle_passes(float2* __restrict__ buf, i
             const int base = blk * L + j;
             float2 v[16];
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = ptr[cpad(base + r * S)];
+            for (int r = 0; r < 16; ++r) v[r] = ptr[CLayout<K, SW>::idx(base + r * S)];
             dft_reg<16>(v);
             twiddle_pow<16>(v, j, L);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) ptr[cpad(base + r * S)] = v[r];
+            for (int r = 0; r < 16; ++r) ptr[CLayout<K, SW>::idx(base + r * S)] = v[r];
         }
         __syncthreads();
-        coarse_middle_passes<K, S>(buf, PG, tid);
+        coarse_middle_passes<K, S, NT, SW>(buf, PG, tid);
     }
 }
 
-// grid: (M / PG, c_count); block kCoarseThreads; dynamic smem = coarse_smem_bytes
+// grid: (M / PG, c_count); block coarse_threads<OUT16>(); dynamic smem = coarse_smem_bytes
 template <int K, int OUT16>
-__global__ void __launch_bounds__(kCoarseThreads, 1) coarse_rm_kernel(CoarseArgs a) {
+__global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT16>())
+    coarse_rm_kernel(CoarseArgs a) {
+    constexpr int NT = coarse_threads<OUT16>();
+    constexpr bool SW = coarse_swizzled<K, OUT16>();
     extern __shared__ float2 smem[];
-    constexpr int Kp = coarse_kp(K);
-    const int PG = coarse_pg_for(K, a.M);
+    constexpr int Kp = CLayout<K, SW>::kp;
+    const int PG = coarse_pg_for(K, a.M, OUT16);
     const int lg_pg = __ffs(PG) - 1;
     float2* buf = smem;
-    float2* s_pre = smem + PG * Kp;
-    int* s_shift = reinterpret_cast<int*>(s_pre + PG);
+    int* s_shift = reinterpret_cast<int*>(smem + PG * Kp);
     float* s_ra = reinterpret_cast<float*>(s_shift + PG);
     float* s_rb = s_ra + PG;
+    float* s_pre = s_rb + PG;
 
     const int tid = threadIdx.x;
     const int m0 = blockIdx.x * PG;
     const unsigned long long c = a.c_begin + blockIdx.y;
 
-    for (int q = tid; q < PG; q += kCoarseThreads) {
+    for (int q = tid; q < PG; q += NT) {
         const int m = m0 + q;
         const double t = static_cast<double>(m + 1) * a.inv_prf;
         const double* cp = a.cparams + 4 * c;
@@ -239,10 +255,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_rm_kernel(CoarseArgs
         s_ra[q] = static_cast<float>(6.283185307179586 * frac / K);
         s_rb[q] = static_cast<float>(b);
         const double cyc = s_predfm * a.two_over_lambda;  // 4pi/lambda * S = 2pi * (2S/lambda)
-        const double fr = cyc - rint(cyc);
-        double ps, pc;
-        sincospi(2.0 * fr, &ps, &pc);
-        s_pre[q] = make_float2(static_cast<float>(pc), static_cast<float>(ps));
+        s_pre[q] = static_cast<float>(6.283185307179586 * (cyc - rint(cyc)));
     }
     __syncthreads();
 
@@ -251,11 +264,12 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_rm_kernel(CoarseArgs
         constexpr int S = K / 16;
         const int total = PG * S;
 #pragma unroll 1
-        for (int i0 = tid; i0 < total; i0 += 2 * kCoarseThreads) {
-            float2 v[2][16];
+        constexpr int H = OUT16 ? 2 : 1;  // butterflies in flight per thread (register budget)
+        for (int i0 = tid; i0 < total; i0 += H * NT) {
+            float2 v[H][16];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int idx = i0 + h * kCoarseThreads;
+            for (int h = 0; h < H; ++h) {
+                const int idx = i0 + h * NT;
                 if (idx < total) {
                     const int p = idx / S;
                     const int j = idx - p * S;
@@ -265,40 +279,48 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_rm_kernel(CoarseArgs
                 }
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int idx = i0 + h * kCoarseThreads;
+            for (int h = 0; h < H; ++h) {
+                const int idx = i0 + h * NT;
                 if (idx < total) {
                     const int p = idx / S;
                     const int j = idx - p * S;
-                    const float ra = s_ra[p], rb = s_rb[p];
+                    const float ra = s_ra[p], rb = s_rb[p], pre = s_pre[p];
+                    const int sp = s_shift[p];
+                    // integer shift in cycles, exact: ((j + r S) s mod K) / K = c0 + r c1 (mod 1)
+                    constexpr float kInvK = 1.0f / static_cast<float>(K);
+                    const float c0 = static_cast<float>((j * sp) & (K - 1)) * kInvK;
+                    const float c1 = static_cast<float>((S * sp) & (K - 1)) * kInvK;
+                    const float fj = static_cast<float>(j);
 #pragma unroll
                     for (int r = 0; r < 16; ++r) {
-                        const int k = j + r * S;
-                        const float gg = static_cast<float>(k < K / 2 ? k : k - K);
+                        const float gg = fj + static_cast<float>(r < 8 ? r * S : r * S - K);  // g(k), k = j + r S
+                        const float cyc = fmaf(static_cast<float>(r), c1, c0);
+                        const float ti = cyc - rintf(cyc);
                         float sn, cs;
-                        __sincosf(fmaf(rb * gg, gg, ra * gg), &sn, &cs);
+                        __sincosf(fmaf(6.28318530717958647692f, ti, fmaf(rb * gg, gg, fmaf(ra, gg, pre))), &sn, &cs);
                         v[h][r] = cmul(v[h][r], make_float2(cs, sn));
                     }
                     dft_reg<16>(v[h]);
                     if constexpr (S > 1) twiddle_pow<16>(v[h], j, K);
                     float2* dst = buf + p * Kp;
 #pragma unroll
-                    for (int r = 0; r < 16; ++r) dst[cpad(j + r * S)] = v[h][r];
+                    for (int r = 0; r < 16; ++r) dst[CLayout<K, SW>::idx(j + r * S)] = v[h][r];
                 }
             }
         }
         __syncthreads();
     }
-    coarse_middle_passes<K, K / 16>(buf, PG, tid);
+    coarse_middle_passes<K, K / 16, NT, SW>(buf, PG, tid);
 
     const float sc = OUT16 ? fp16_prescale(a.maxbits, K) : 1.0f;
     constexpr int RL = K == 16 ? 1 : coarse_last_radix(K);
-    coarse_last_pass<K, RL, OUT16>(a, buf, PG, lg_pg, s_shift, s_pre, sc, tid);
+    coarse_last_pass<K, RL, OUT16, NT, SW>(a, buf, PG, lg_pg, sc, tid);
 }
 
-inline size_t coarse_smem_bytes(int K, int M) {
-    const int PG = coarse_pg_for(K, M);
-    return static_cast<size_t>(PG) * coarse_kp(K) * sizeof(float2) + static_cast<size_t>(PG) * (8 + 4 + 4 + 4);
+inline size_t coarse_smem_bytes(int K, int M, int out16 = 1) {
+    const int PG = coarse_pg_for(K, M, out16);
+    const int kp = (K == 2048 && !out16) ? CLayout<2048, true>::kp : coarse_kp(K);
+    return static_cast<size_t>(PG) * kp * sizeof(float2) + static_cast<size_t>(PG) * (4 + 4 + 4 + 4);
 }
 
 // f64 interleaved host layout -> complex64 device cube

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda.h>
 
 #include "../../include/ltci_cuda.h"
 #include "coarse.cuh"
@@ -329,13 +330,55 @@ void ensure_smem_attr(const void* kern, int bytes) {
 
 int coarse_pg(int K, int M) { return coarse_pg_for(K, M); }
 
+__global__ void module_anchor_kernel() {}
+
+// The runtime loads kernels lazily, on their first launch, so module-loading
+// time would land in whichever detector call first needs an instantiation
+// (a latency spike inside a timed or real-time call).  The first engine on a
+// device therefore loads every function of this module up front through the
+// driver's module enumeration; best effort: any failure leaves lazy loading.
+void preload_module() {
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.insert(dev).second) return;
+    using GetModule = CUresult (*)(CUmodule*, CUfunction);
+    using Count = CUresult (*)(unsigned int*, CUmodule);
+    using Enumerate = CUresult (*)(CUfunction*, unsigned int, CUmodule);
+    using Load = CUresult (*)(CUfunction);
+    void *p_mod = nullptr, *p_cnt = nullptr, *p_enum = nullptr, *p_load = nullptr;
+    if (cudaGetDriverEntryPoint("cuFuncGetModule", &p_mod, cudaEnableDefault) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuModuleGetFunctionCount", &p_cnt, cudaEnableDefault) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuModuleEnumerateFunctions", &p_enum, cudaEnableDefault) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuFuncLoad", &p_load, cudaEnableDefault) != cudaSuccess || !p_mod || !p_cnt ||
+        !p_enum || !p_load) {
+        cudaGetLastError();
+        return;
+    }
+    cudaFunction_t anchor = nullptr;
+    if (cudaGetFuncBySymbol(&anchor, reinterpret_cast<const void*>(module_anchor_kernel)) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    CUmodule mod = nullptr;
+    unsigned int n = 0;
+    if (reinterpret_cast<GetModule>(p_mod)(&mod, reinterpret_cast<CUfunction>(anchor)) != CUDA_SUCCESS ||
+        reinterpret_cast<Count>(p_cnt)(&n, mod) != CUDA_SUCCESS || n == 0)
+        return;
+    std::vector<CUfunction> fns(n);
+    if (reinterpret_cast<Enumerate>(p_enum)(fns.data(), n, mod) != CUDA_SUCCESS) return;
+    for (CUfunction f : fns) reinterpret_cast<Load>(p_load)(f);
+}
+
 template <int K, int OUT16>
 void launch_coarse_k(const CoarseArgs& a, cudaStream_t st) {
     auto kern = coarse_rm_kernel<K, OUT16>;
-    const size_t smem = coarse_smem_bytes(K, a.M);
+    const size_t smem = coarse_smem_bytes(K, a.M, OUT16);
     ensure_smem_attr(reinterpret_cast<const void*>(kern), 160 * 1024);
-    dim3 grid(a.M / coarse_pg_for(K, a.M), a.c_count);
-    kern<<<grid, kCoarseThreads, smem, st>>>(a);
+    dim3 grid(a.M / coarse_pg_for(K, a.M, OUT16), a.c_count);
+    kern<<<grid, coarse_threads<OUT16>(), smem, st>>>(a);
     CK(cudaGetLastError());
 }
 
@@ -434,15 +477,35 @@ void launch_tc_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& 
     CK(cudaGetLastError());
 }
 
-template <int Q, int G, bool DENSE>
-void launch_fine_tm(const FineArgs& a, cudaStream_t st) {
+// Doppler-window blocks: the smallest NB in {3, 6} with every needed bin in the
+// first or last NB 32-bin blocks, else 0 (any window, e.g. DS-KT-MFP's full axis)
+inline int fine_window_nb(const FineArgs& a, int Q, int G) {
+    const int nbp = a.kA >= 0 ? a.kA / Q + 1 : 0;
+    const int nbn = a.kB <= Q * G - 1 ? G - a.kB / Q : 0;
+    const int nb = std::max(nbp, nbn);
+    if (std::getenv("LTCI_FINE_NOPRUNE")) return 0;
+    return nb <= 3 ? 3 : nb <= 6 ? 6 : 0;
+}
+
+template <int Q, int G, bool DENSE, int NB>
+void launch_fine_tm_nb(const FineArgs& a, cudaStream_t st) {
     const size_t smem = fine_tm_smem_floats2<Q, G>() * sizeof(float2);
-    auto kern = fine_fft_tm_kernel<Q, G, DENSE>;
+    auto kern = fine_fft_tm_kernel<Q, G, DENSE, NB>;
     ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     constexpr int rows_per_block = fine_tm_warps<Q, G>() * (32 / G);
     const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
     kern<<<blocks, fine_tm_warps<Q, G>() * 32, smem, st>>>(a);
     CK(cudaGetLastError());
+}
+
+template <int Q, int G, bool DENSE>
+void launch_fine_tm(const FineArgs& a, cudaStream_t st) {
+    if constexpr (G >= 16) {
+        const int nb = 2 * fine_window_nb(a, Q, G) <= G ? fine_window_nb(a, Q, G) : 0;
+        if (nb == 3) return launch_fine_tm_nb<Q, G, DENSE, 3>(a, st);
+        if (nb == 6) return launch_fine_tm_nb<Q, G, DENSE, 6>(a, st);
+    }
+    launch_fine_tm_nb<Q, G, DENSE, 0>(a, st);
 }
 
 template <int Q, int G, bool DENSE>
@@ -559,6 +622,7 @@ void engine_init(ltci_engine* e) {
         fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
     if (e->device < 0 || e->device >= ndev) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad device ordinal");
     DeviceGuard dg(e->device);
+    preload_module();
     e->cparams.ensure(pl.cparams.size());
     CK(cudaMemcpy(e->cparams.p, pl.cparams.data(), pl.cparams.size() * sizeof(double), cudaMemcpyHostToDevice));
     e->h0.ensure(pl.h0.size());
@@ -1067,6 +1131,7 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
         fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
     if (device < 0 || device >= ndev) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad device ordinal");
     DeviceGuard dg(device);
+    preload_module();
     cudaStream_t st = nullptr;
     const int K = rp.K, M = rp.M;
     const size_t n = static_cast<size_t>(K) * M;
