@@ -455,9 +455,11 @@ def main():
             per_launch_flops = coarse * rows_here * fine_cells * fft_flops_per_row_cell(p.M, D)
             achieved = per_launch_flops / fine_s / 1e12
             tm = p.M == 1024
+            kname = ("fine_fft_tm_kernel (K2b+K3, CUDA cores, TMEM-resident rows)" if 256 <= p.M <= 1024 else
+                     "fine_fft_tm2k_kernel (K2b+K3, CUDA cores, radix-2 split onto two TMEM 1024-point halves)"
+                     if p.M == 2048 else "fine_fft_kernel (K2b+K3, CUDA cores)")
             roof = {"bound": "fp32",
-                    "kernel": "fine_fft_tm_kernel (K2b+K3, CUDA cores, TMEM-resident rows)" if tm
-                    else "fine_fft_kernel (K2b+K3, CUDA cores)",
+                    "kernel": kname,
                     "achieved": achieved, "peak": fp32.value, "unit": "TFLOP/s",
                     "frac": achieved / fp32.value if fp32.value else None,
                     "traffic": _ncu_traffic(args.config, "fine_fft_tm_kernel<0>") if tm else None,

@@ -148,6 +148,7 @@ __device__ __forceinline__ void coarse_last_pass(const CoarseArgs& a, const floa
     const int total = PG * G;
     const size_t cbase = static_cast<size_t>(blockIdx.y) * a.R_slice * a.M;
     const int m0 = blockIdx.x * PG;
+    const bool full = a.n_base == 0 && a.R_slice == K;  // ROI = all range cells, one slice
     for (int idx = tid; idx < total; idx += NT) {
         const int p = idx & (PG - 1);  // lanes run over pulses first: one row per PG lanes
         const int kl = idx >> lg_pg;   // this thread's bins: kl + G t
@@ -157,6 +158,14 @@ __device__ __forceinline__ void coarse_last_pass(const CoarseArgs& a, const floa
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = src[CLayout<K, SW>::idx(pos0 + r)];
         dft_reg<R>(v);
+        if (!OUT16 && full) {
+            // every bin is a stored row (n = bin): rows kl + G t, one pointer
+            float2* dst = a.X + cbase + static_cast<size_t>(kl) * a.M + m0 + p;
+            const size_t step = static_cast<size_t>(G) * a.M;
+#pragma unroll
+            for (int t = 0; t < R; ++t) dst[t * step] = v[t];
+            continue;
+        }
 #pragma unroll
         for (int t = 0; t < R; ++t) {
             const int n = (kl + G * t - a.n_base) & (K - 1);  // row of bin kl + G t

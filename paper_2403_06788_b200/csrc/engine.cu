@@ -190,11 +190,11 @@ void check_grids(const ltci_dual_space& s) {
 }
 
 void check_supported(const ltci_radar& r, int fine_path = LTCI_FINE_AUTO) {
-    // CUDA-core FFT path: M in [4, 1024]; tcgen05 path: M in [32, 2048]
-    const bool tc = fine_path == LTCI_FINE_TC_DENSE || fine_path == LTCI_FINE_TC_FAST ||
-                    (fine_path == LTCI_FINE_AUTO && r.M > 1024);
-    if (r.M < 4 || r.M > 2048 || (!tc && r.M > 1024) || (tc && r.M < 32))
-        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: pulse count M must be a power of two in [4, 1024] "
+    // CUDA-core FFT path: M in [4, 2048] (M = 2048 for Doppler-windowed
+    // searches, checked at launch); tcgen05 path: M in [32, 2048]
+    const bool tc = fine_path == LTCI_FINE_TC_DENSE || fine_path == LTCI_FINE_TC_FAST;
+    if (r.M < 4 || r.M > 2048 || (tc && r.M < 32))
+        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: pulse count M must be a power of two in [4, 2048] "
                                     "(CUDA-core path) or [32, 2048] (tcgen05 path)");
     if (r.K < 16 || r.K > 8192)
         fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be a power of two in [16, 8192]");
@@ -525,8 +525,34 @@ void launch_fine_qg(const FineArgs& a, cudaStream_t st) {
     CK(cudaGetLastError());
 }
 
+// M = 2048 (fine_fft_tm2k_kernel): NB over the half-length (1024-bin) axes of
+// the even and odd output bins; 0 = window too wide for the kernel
+inline int tm2k_nb(int kA, int kB) {
+    const int nbp = kA >= 0 ? (kA / 2) / 32 + 1 : 0;
+    const int nbn = kB <= 2047 ? 32 - ((kB - 1) / 2) / 32 : 0;
+    const int nb = std::max(nbp, nbn);
+    return nb <= 3 ? 3 : nb <= 6 ? 6 : 0;
+}
+
+template <bool DENSE, int NB>
+void launch_fine_tm2k_nb(const FineArgs& a, cudaStream_t st) {
+    auto kern = fine_fft_tm2k_kernel<DENSE, NB>;
+    const int smem = fine_tm2k_smem_bytes();
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+    const int blocks = (a.rows + kTm2kWarps - 1) / kTm2kWarps;
+    kern<<<blocks, kTm2kWarps * 32, smem, st>>>(a);
+    CK(cudaGetLastError());
+}
+
 template <bool DENSE>
 void launch_fine_m(const FineArgs& a, int M, cudaStream_t st) {
+    if (M == 2048) {
+        const int nb = tm2k_nb(a.kA, a.kB);
+        if (nb == 3) return launch_fine_tm2k_nb<DENSE, 3>(a, st);
+        if (nb == 6) return launch_fine_tm2k_nb<DENSE, 6>(a, st);
+        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: CUDA-core fine path at M = 2048 needs a Doppler window of "
+                                    "at most 12 x 64 bins (use the tcgen05 path)");
+    }
     switch (M) {
         case 4: launch_fine_qg<4, 1, DENSE>(a, st); break;
         case 8: launch_fine_qg<8, 1, DENSE>(a, st); break;

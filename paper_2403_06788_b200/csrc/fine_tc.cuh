@@ -833,9 +833,17 @@ inline bool tc_fine_selected(int fine_path, int M, int D, bool keep_dense) {
     // AUTO (by measurement): M = 256..1024 runs the CUDA-core
     // FFT path with TMEM-resident rows (C1: 222 vs 246 ms tensor 3-term; C4:
     // 8.7 vs 12.3 ms per CPI; C0: 0.56 vs 0.69 ms; C3 KT, D = M: the dense
-    // form is ~8x the work); M > 1024 has only the tensor path; below 256 the
+    // form is ~8x the work); M = 2048 likewise for a narrow window; below 256 the
     // 3-term (FP32-class) tensor path for a narrow Doppler window, else FFT.
     if (M >= 256 && M <= 1024) return false;
+    if (M == 2048) {
+        // CUDA-core FFT (radix-2 split onto two 1024-point halves) when the
+        // Doppler window fits its pruned second pass (symmetric window of D
+        // bins: at most 6 32-bin blocks per side of each half axis)
+        const int keep = (D - 1) / 2;
+        const int nbp = (keep / 2) / 32 + 1, nbn = 32 - ((M - keep - 1) / 2) / 32;
+        return std::max(nbp, nbn) > 6;
+    }
     if (keep_dense) return M > 1024;
     return M > 1024 || (M >= 64 && (D <= 160 || 2 * D <= M));
 }

@@ -110,5 +110,5 @@ def test_fine_path_selection_is_honoured():
     e.close()
     w2 = config(2)
     e = Engine(w2.params, w2.space, opt=DetectorOptions())
-    assert e.fine_path()[0] == A.FINE_TC_DENSE  # M = 2048: tensor path only
+    assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE  # M = 2048, D = 151: radix-2 split FFT path
     e.close()

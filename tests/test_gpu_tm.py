@@ -114,3 +114,50 @@ def test_roi_edges_both_paths(path, roi):
     assert max_rel(gm.dense, rm.dense) <= TOL
     check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, 0.2 * M)
     check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
+
+
+CASES_2K = [  # M = 2048 (fine_fft_tm2k_kernel: radix-2 split onto two 1024-point halves)
+    (1, [(-10.0, 10.0)], [1.0]),
+    (2, [(-10.0, 10.0), (-1.0, 1.0)], [0.5, 0.5]),
+    (3, [(-6.0, 6.0), (-0.6, 0.6), (-0.1, 0.1)], [0.4, 0.3, 0.3]),
+]
+
+
+@pytest.mark.parametrize("P,bounds,alpha", CASES_2K)
+def test_tm2k_fft_dense_vs_oracle(P, bounds, alpha):
+    p, s, x = _setup(2048, P, bounds, alpha)
+    retain = 0.3 * 2048.0
+    opt = DetectorOptions(retain_threshold=retain, keep_dense=True)
+    e = Engine(p, s, opt=opt)
+    assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE
+    e.run_host(x)
+    gm = e.result()
+    e.close()
+    rm = O.port_ds(x, p, s, opt)
+    assert gm.counters == rm.counters
+    assert max_rel(gm.dense, rm.dense) <= TOL
+    check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, retain)
+    check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
+
+
+@pytest.mark.parametrize("fc_over_fs", [150.0, 800.0])
+def test_tm2k_wide_window_vs_oracle(fc_over_fs):
+    """Doppler windows of 77 and ~400 bins (the NB = 3 and NB = 6 pruned
+    second passes over both half axes), candidates and per-cell peaks."""
+    M, K = 2048, 64
+    fs = 20e6
+    p = RadarParams.create(fc_over_fs * fs, fs, fs, 1000.0, M, K)
+    s = build_dual_scale(p, 2, [Bounds(-15.0, 15.0), Bounds(-1.0, 1.0)], [0.5, 0.5], RangeRoi(20, 27))
+    x = scene.to_complex64_roundtrip(scene.add_noise(
+        scene.synthesize_cube(p, [(0.02, [23 * p.delta_R(), 11.0, 0.2])]), 1.0 / K, 2048 + int(fc_over_fs)))
+    retain = 0.25 * M
+    opt = DetectorOptions(retain_threshold=retain)
+    e = Engine(p, s, opt=opt)
+    assert e.fine_path()[0] == A.FINE_FFT_CUDA_CORE
+    e.run_host(x)
+    gm = e.result()
+    e.close()
+    rm = O.port_ds(x, p, s, opt)
+    assert gm.counters == rm.counters and gm.argmax == rm.argmax
+    check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, retain)
+    check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value)
