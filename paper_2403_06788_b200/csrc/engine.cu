@@ -109,6 +109,7 @@ struct Plan {
     std::vector<int> fine_orders;        // motion order of each fine axis
     unsigned long long fine_cells = 1;
     int n_outer = 1, n_inner = 1;
+    int n_split = 1, chunk = 1;           // inner fine axis split across CTAs (small grids)
     int R_total = 0, roi_first = 0;
     int row_begin = 0, row_end = 0, R_slice = 0;
     int D = 0, dop_first = 0;
@@ -137,13 +138,32 @@ void build_fine_tables(Plan& pl) {
     pl.n_inner = nf > 0 ? pl.fine_axes[nf - 1].count : 1;
     pl.n_outer = 1;
     for (int i = 0; i + 1 < nf; ++i) pl.n_outer *= pl.fine_axes[i].count;
-    pl.h0.assign(static_cast<size_t>(pl.n_outer) * M, make_float2(1.f, 0.f));
+    pl.n_split = 1;
+    pl.chunk = pl.n_inner;
+    // Small problems (C0: 11 coarse cells x 512 rows = 1 408 warps of the
+    // M = 256 TMEM kernel, under one wave of 148 SMs x 16 warps) split the
+    // inner fine axis across CTAs: chunk sp starts from its own FP64 seed.
+    if (nf > 0 && M >= 256 && M <= 1024 && !tc_fine_selected(pl.fine_path, M, pl.D, pl.keep_dense) &&
+        !std::getenv("LTCI_FINE_NOSPLIT")) {
+        // global sizes only (R_total, not the slice): every shard picks the same split, so
+        // range-cell shards still reproduce the 1-GPU map bit for bit
+        const double warps = static_cast<double>(pl.coarse_cells) * pl.R_total * M / 1024.0;
+        const double want = 148.0 * 16.0 * 3.0;
+        int ns = static_cast<int>(std::ceil(want / std::max(1.0, warps)));
+        ns = std::max(1, std::min(ns, pl.n_inner / 16));
+        if (ns > 1) {
+            pl.chunk = (pl.n_inner + ns - 1) / ns;
+            pl.n_split = (pl.n_inner + pl.chunk - 1) / pl.chunk;
+        }
+    }
+    pl.h0.assign(static_cast<size_t>(pl.n_outer) * pl.n_split * M, make_float2(1.f, 0.f));
     pl.hstep.assign(M, make_float2(1.f, 0.f));
     if (nf == 0) return;
-    for (int outer = 0; outer < pl.n_outer; ++outer) {
+    for (int outer = 0; outer < pl.n_outer * pl.n_split; ++outer) {
+        const int sp = outer % pl.n_split;
         // decode outer over fine axes 0..nf-2 (last fastest)
         std::vector<int> fi(nf, 0);
-        int rem = outer;
+        int rem = outer / pl.n_split;
         for (int i = nf - 2; i >= 0; --i) {
             fi[i] = rem % pl.fine_axes[i].count;
             rem /= pl.fine_axes[i].count;
@@ -153,7 +173,7 @@ void build_fine_tables(Plan& pl) {
             double s = 0.0;
             for (int i = 0; i < nf; ++i) {
                 const double val = i + 1 < nf ? pl.fine_axes[i].start + pl.fine_axes[i].step * fi[i]
-                                              : pl.fine_axes[i].start;
+                                              : pl.fine_axes[i].start + pl.fine_axes[i].step * (sp * pl.chunk);
                 s += pl.kappa * val * std::pow(t, pl.fine_orders[i]);
             }
             pl.h0[static_cast<size_t>(outer) * M + m] = phase_lambda(s, lam);
@@ -494,7 +514,7 @@ void launch_fine_tm_nb(const FineArgs& a, cudaStream_t st) {
     ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     constexpr int rows_per_block = fine_tm_warps<Q, G>() * (32 / G);
     const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
-    kern<<<blocks, fine_tm_warps<Q, G>() * 32, smem, st>>>(a);
+    kern<<<dim3(blocks, a.n_split), fine_tm_warps<Q, G>() * 32, smem, st>>>(a);
     CK(cudaGetLastError());
 }
 
@@ -516,6 +536,7 @@ void launch_fine_qg(const FineArgs& a, cudaStream_t st) {
             return;
         }
     }
+    if (a.n_split != 1) fail(LTCI_RUNTIME_ERROR, "ltci_cuda: fine-axis split on a kernel without it");
     constexpr int rows_per_block = (kFineThreads / 32) * (32 / G);
     const size_t smem = fine_smem_floats2<Q, G>() * sizeof(float2);
     auto kern = fine_fft_kernel<Q, G, DENSE>;
@@ -778,6 +799,8 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
     }
     fa.n_outer = pl.n_outer;
     fa.n_inner = pl.n_inner;
+    fa.n_split = pl.n_split;
+    fa.chunk = pl.chunk;
     {
         const double r2 = pl.retain * pl.retain;
         fa.retain2 = pl.retain < 0 ? -1.0f : static_cast<float>(r2);
@@ -1553,6 +1576,8 @@ int ltci_cuda_gft(const double* rows, const ltci_radar* p, const double* fine_hi
         fa.kB = M / 2;
         fa.n_outer = 1;
         fa.n_inner = 1;
+        fa.n_split = 1;
+        fa.chunk = 1;
         fa.retain2 = INFINITY;
         launch_fine_m<true>(fa, M, nullptr);
         std::vector<float2> hd(static_cast<size_t>(R) * M);

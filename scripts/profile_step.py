@@ -15,10 +15,11 @@ ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--runs", type=int, default=1)
 ap.add_argument("--fine-path", default="auto", choices=["auto", "fft", "tc", "tcfast"])
 ap.add_argument("--coarse-v", type=int, default=0, help="slice the coarse velocity axis")
+ap.add_argument("--coarse-rest", type=int, default=0, help="with --coarse-v: also slice the other coarse axes")
 a = ap.parse_args()
 w = configs.config(a.config)
 if a.coarse_v:
-    w = configs.sliced(w, a.coarse_v)
+    w = configs.sliced(w, a.coarse_v, a.coarse_rest)
 fp = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE, "tcfast": A.FINE_TC_FAST}[a.fine_path]
 opt = DetectorOptions(retain_threshold=detection_threshold(w.params, w.sigma2, 1e-6), fine_path=fp)
 e = Engine(w.params, w.space, w.variant, w.amb, opt)
