@@ -520,7 +520,7 @@ void launch_fine_tm_nb(const FineArgs& a, cudaStream_t st) {
 
 template <int Q, int G, bool DENSE>
 void launch_fine_tm(const FineArgs& a, cudaStream_t st) {
-    if constexpr (G >= 16) {
+    if constexpr (G >= 8) {
         const int nb = 2 * fine_window_nb(a, Q, G) <= G ? fine_window_nb(a, Q, G) : 0;
         if (nb == 3) return launch_fine_tm_nb<Q, G, DENSE, 3>(a, st);
         if (nb == 6) return launch_fine_tm_nb<Q, G, DENSE, 6>(a, st);

@@ -1,5 +1,5 @@
 # quick GPU check: the TMEM FFT parity tests + C4/C1 bench lines
 set -x
 timeout 900 python -m pytest tests/test_gpu_tm.py tests/test_gpu_parity.py -x -q > gpurun_out/q_tests.log 2>&1
-python bench.py --no-cpu-baseline --config 4 > gpurun_out/q_c4.log 2>&1
+python bench.py --no-cpu-baseline --config 0 > gpurun_out/q_c0.log 2>&1
 python bench.py --no-cpu-baseline > gpurun_out/q_c1.log 2>&1
