@@ -97,12 +97,14 @@ def test_c4_one_cpi_full_size():
     _cross_and_oracle(w, x, gamma, samples=6, seed=4)
 
 
-def test_c1_range_shards_merge_bit_exactly():
-    """C1 on the TMEM-resident FFT path split into 3 uneven range-cell shards
-    (the multi-GPU partition, one engine per GPU) merges to the 1-GPU map
+@pytest.mark.parametrize("cfg", [1, 0])
+def test_range_shards_merge_bit_exactly(cfg):
+    """C1 (and C0, whose small grid splits the inner fine axis across CTAs) on
+    the TMEM-resident FFT path split into 3 uneven range-cell shards (the
+    multi-GPU partition, one engine per GPU) merges to the 1-GPU map
     bit-exactly; parallel.merge_rank_maps is the merge the NCCL gather feeds."""
     from paper_2403_06788_b200.parallel import merge_rank_maps, shard_rows
-    w = config(1)
+    w = config(cfg)
     x = scene.to_complex64_roundtrip(w.cube())
     gamma = detection_threshold(w.params, w.sigma2, 1e-6)
     opt = DetectorOptions(retain_threshold=gamma)
@@ -131,7 +133,7 @@ def test_coarse_shards_merge_bit_exactly(cfg):
     disjoint coarse-cell slices, every ROI row; their raw peak slots merged on
     the device (ltci_cuda_merge_peaks) equal the 1-GPU slots bit for bit, the
     candidate union equals the 1-GPU candidates, the host merge agrees.
-    C1 runs the TMEM FFT path, C0 the tensor path."""
+    Both run the TMEM FFT path (C0 with its fine-axis split)."""
     import ctypes as C
 
     import torch
