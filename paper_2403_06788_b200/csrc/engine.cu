@@ -687,6 +687,12 @@ void engine_init(ltci_engine* e) {
     e->batch = std::min<unsigned long long>(e->batch, (1ull << 30) / std::max(1, pl.R_slice));
     e->use_tc = tc_fine_selected(pl.fine_path, M, pl.D, pl.keep_dense);
     e->tc_terms = tc_terms_for(pl.fine_path);
+    if (!e->use_tc && M == 2048) {
+        const int dlo = pl.dop_first - M / 2;
+        if (tm2k_nb(dlo + pl.D - 1, M + dlo) == 0)
+            fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: CUDA-core fine path at M = 2048 needs a Doppler window of "
+                                        "at most 12 x 64 bins (use the tcgen05 path)");
+    }
     if (e->use_tc) {
         const size_t words = e->batch * static_cast<size_t>(pl.R_slice) * M;  // one half2 per complex sample
         e->x16h.ensure(words);
@@ -1082,9 +1088,21 @@ int detect(const double* cube, const ltci_radar* cp, const ltci_ambiguity* amb, 
            const ltci_options* opt, int variant, ltci_detection_map** out) {
     return guarded([&] {
         if (!cube || !cp || !s || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
-        ltci_engine eng;
+        const int device = opt ? opt->device : 0;
+        if (device < 0) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad device ordinal");
+        // One-shot calls reuse a per-thread, per-device engine: its device
+        // buffers only grow, so a stream of small calls (Monte-Carlo trials,
+        // the reference's timing loops) pays no cudaMalloc/cudaFree per call.
+        thread_local std::vector<std::unique_ptr<ltci_engine>> pool;
+        if (static_cast<int>(pool.size()) <= device) pool.resize(device + 1);
+        if (!pool[device]) pool[device] = std::make_unique<ltci_engine>();
+        ltci_engine& eng = *pool[device];
         eng.pl = make_plan(*cp, *s, amb, variant, opt, 0, -1);
-        eng.device = opt ? opt->device : 0;
+        eng.device = device;
+        eng.htab_ready = false;  // the chirp table belongs to the previous plan
+        eng.c_lo = 0;
+        eng.c_hi = ~0ull;
+        eng.timing = false;
         engine_init(&eng);
         DeviceGuard dg(eng.device);
         cudaStream_t st = nullptr;

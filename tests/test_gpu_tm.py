@@ -161,3 +161,17 @@ def test_tm2k_wide_window_vs_oracle(fc_over_fs):
     assert gm.counters == rm.counters and gm.argmax == rm.argmax
     check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, retain)
     check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value)
+
+
+def test_tm2k_full_axis_path_choice():
+    """DS-KT-MFP keeps the whole Doppler axis: at M = 2048 AUTO runs the tensor
+    path and an explicit CUDA-core request fails at engine creation."""
+    M, K = 2048, 64
+    p = RadarParams.create(8 * 100e6, 100e6, 50e6, 2000.0, M, K)
+    s = build_dual_scale(p, 2, [Bounds(-10.0, 10.0), Bounds(-1.0, 1.0)], [0.5, 0.5], RangeRoi(2, K - 3))
+    amb = build_ambiguity(p, Bounds(-1.6 * p.Va(), 1.6 * p.Va()))
+    e = Engine(p, s, 1, amb, DetectorOptions())
+    assert e.fine_path()[0] == A.FINE_TC_DENSE
+    e.close()
+    with pytest.raises(ValueError):
+        Engine(p, s, 1, amb, DetectorOptions(fine_path=A.FINE_FFT_CUDA_CORE))
