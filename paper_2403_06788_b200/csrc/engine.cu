@@ -10,6 +10,7 @@
 // predict_counters (proj/src/bench.cpp:180-189).
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -737,7 +738,9 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
     // slots: re = im = 0, idx = ~0 (on the stream: run_device never blocks the host)
     init_slots_kernel<<<std::max(1, std::min(148, (pl.R_slice + 255) / 256)), 256, 0, st>>>(e->slots.p, pl.R_slice);
     CK(cudaGetLastError());
-    if (pl.keep_dense) CK(cudaMemsetAsync(e->dense.p, 0, e->dense.n * sizeof(float2), st));
+    if (pl.keep_dense)
+        CK(cudaMemsetAsync(e->dense.p, 0,
+                           static_cast<size_t>(pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D) * sizeof(float2), st));
 
     const float2* input = d_cube;
     if (pl.variant == LTCI_VARIANT_KTMFP) {
@@ -1035,7 +1038,7 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         CK(cudaMemcpyAsync(slots.data(), e->slots.p, slots.size() * sizeof(PeakSlot), cudaMemcpyDeviceToHost, st));
         std::vector<float2> dense;
         if (pl.keep_dense) {
-            dense.resize(e->dense.n);
+            dense.resize(static_cast<size_t>(pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D));  // not the (grow-only) buffer
             CK(cudaMemcpyAsync(dense.data(), e->dense.p, dense.size() * sizeof(float2), cudaMemcpyDeviceToHost, st));
         }
         CK(cudaStreamSynchronize(st));
@@ -1097,18 +1100,34 @@ int detect(const double* cube, const ltci_radar* cp, const ltci_ambiguity* amb, 
         if (static_cast<int>(pool.size()) <= device) pool.resize(device + 1);
         if (!pool[device]) pool[device] = std::make_unique<ltci_engine>();
         ltci_engine& eng = *pool[device];
+        static const bool trace = std::getenv("LTCI_TRACE") != nullptr;  // per-phase wall times on stderr
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
         eng.pl = make_plan(*cp, *s, amb, variant, opt, 0, -1);
         eng.device = device;
         eng.htab_ready = false;  // the chirp table belongs to the previous plan
         eng.c_lo = 0;
         eng.c_hi = ~0ull;
         eng.timing = false;
+        const auto t1 = clk::now();
         engine_init(&eng);
+        const auto t2 = clk::now();
         DeviceGuard dg(eng.device);
         cudaStream_t st = nullptr;
         upload_host_cube(&eng, cube, st);
         run_device_impl(&eng, eng.cube_c64.p, st);
+        if (trace) CK(cudaStreamSynchronize(st));
+        const auto t3 = clk::now();
         *out = assemble(&eng, st);
+        if (trace) {
+            const auto t4 = clk::now();
+            auto ms = [](clk::time_point a, clk::time_point b) {
+                return std::chrono::duration<double, std::milli>(b - a).count();
+            };
+            std::fprintf(stderr, "[ltci] %s M=%d K=%d D=%d tc=%d plan %.2f init %.2f run %.2f assemble %.2f ms\n",
+                         variant == LTCI_VARIANT_KTMFP ? "ds_kt_mfp" : "ds_grft", eng.pl.rp.M, eng.pl.rp.K,
+                         eng.pl.D, eng.use_tc ? 1 : 0, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+        }
     });
 }
 
