@@ -300,14 +300,40 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT
                     const float c0 = static_cast<float>((j * sp) & (K - 1)) * kInvK;
                     const float c1 = static_cast<float>((S * sp) & (K - 1)) * kInvK;
                     const float fj = static_cast<float>(j);
-#pragma unroll
-                    for (int r = 0; r < 16; ++r) {
-                        const float gg = fj + static_cast<float>(r < 8 ? r * S : r * S - K);  // g(k), k = j + r S
-                        const float cyc = fmaf(static_cast<float>(r), c1, c0);
-                        const float ti = cyc - rintf(cyc);
+                    if (a.variant == 0) {
+                        // GRFT: the phase is linear in r on each half (g jumps by -K at r = 8),
+                        // so 3 sincos per 16 points: the two half bases and the common step,
+                        // then an 8-long power chain per half (fp32 drift ~1e-6 rel).
+                        constexpr float kTwoPi = 6.28318530717958647692f;
+                        const float cy8 = fmaf(8.0f, c1, c0);
                         float sn, cs;
-                        __sincosf(fmaf(6.28318530717958647692f, ti, fmaf(rb * gg, gg, fmaf(ra, gg, pre))), &sn, &cs);
-                        v[h][r] = cmul(v[h][r], make_float2(cs, sn));
+                        __sincosf(fmaf(kTwoPi, c0 - rintf(c0), fmaf(ra, fj, pre)), &sn, &cs);
+                        float2 w0 = make_float2(cs, sn);
+                        __sincosf(fmaf(kTwoPi, cy8 - rintf(cy8), fmaf(ra, fj + static_cast<float>(8 * S - K), pre)),
+                                  &sn, &cs);
+                        float2 w8 = make_float2(cs, sn);
+                        __sincosf(fmaf(kTwoPi, c1 - rintf(c1), ra * static_cast<float>(S)), &sn, &cs);
+                        const float2 st = make_float2(cs, sn);
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            v[h][r] = cmul(v[h][r], w0);
+                            v[h][r + 8] = cmul(v[h][r + 8], w8);
+                            if (r < 7) {
+                                w0 = cmul(w0, st);
+                                w8 = cmul(w8, st);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < 16; ++r) {
+                            const float gg = fj + static_cast<float>(r < 8 ? r * S : r * S - K);  // g(k), k = j + r S
+                            const float cyc = fmaf(static_cast<float>(r), c1, c0);
+                            const float ti = cyc - rintf(cyc);
+                            float sn, cs;
+                            __sincosf(fmaf(6.28318530717958647692f, ti, fmaf(rb * gg, gg, fmaf(ra, gg, pre))), &sn,
+                                      &cs);
+                            v[h][r] = cmul(v[h][r], make_float2(cs, sn));
+                        }
                     }
                     dft_reg<16>(v[h]);
                     if constexpr (S > 1) twiddle_pow<16>(v[h], j, K);
