@@ -256,9 +256,33 @@ def main():
     from paper_2403_06788_b200.detectors import Engine, detection_threshold
     from paper_2403_06788_b200.model import DetectorOptions
 
+    # LTCI_BENCH_SHARED_GPU=1: functional check of the N-rank path on a 1-GPU box
+    # (every rank on cuda:0, gloo over host copies); its timings mean nothing
+    shared_gpu = ws > 1 and os.environ.get("LTCI_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def all_gather_into(out, inp):
+        if not shared_gpu:
+            dist.all_gather_into_tensor(out, inp)
+            return
+        parts = [torch.empty_like(inp, device="cpu") for _ in range(ws)]
+        dist.all_gather(parts, inp.cpu())
+        out.copy_(torch.cat(parts).view_as(out))
+
+    def all_reduce_max(t):
+        if not shared_gpu:
+            all_reduce_max(t)
+            return
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX)
+        t.copy_(h)
     dev = torch.device("cuda", local)
     p, s = w.params, w.space
     fine_path = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE,
@@ -318,7 +342,7 @@ def main():
         if ws > 1 and shard == "coarse":
             # every rank holds a peak per row: NCCL all-gather of the 16-byte records,
             # then the per-row max on the device with the kernels' tie-break
-            dist.all_gather_into_tensor(gathered, peaks.view(torch.int32))
+            all_gather_into(gathered, peaks.view(torch.int32))
             _lib.raise_for(lib.ltci_cuda_merge_peaks(ctypes.c_void_p(gathered.data_ptr()), ws, R,
                                                      ctypes.c_void_p(merged.data_ptr()), ctypes.c_void_p(sptr)),
                            lib)
@@ -326,7 +350,7 @@ def main():
             # slices differ by at most one row: pad to a common length
             pad = torch.zeros((R // ws + 1, 4), dtype=torch.int32, device=dev)
             pad[:n_rows].copy_(peaks.view(torch.int32))
-            dist.all_gather_into_tensor(gathered, pad)
+            all_gather_into(gathered, pad)
 
     def step_local():
         for i, dc in enumerate(d_cubes):
@@ -372,7 +396,7 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_max(t)
     ms_max = float(t.item())
     total_integ = w.integrations() * cpis  # all ranks together cover every hypothesis of every CPI once
     value = total_integ * args.steps / (ms_max * 1e-3) / 1e9
@@ -408,7 +432,7 @@ def main():
             e2e_ms.append((t1 - t0) * 1e3)
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if ws > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        all_reduce_max(e2e_t)
     e2e_value = total_integ * args.steps / (float(e2e_t.item()) * 1e-3) / 1e9
 
     if rank == 0:
@@ -511,6 +535,22 @@ def main():
             except Exception as e:  # reported, not fatal
                 cb = {"error": str(e)}
             line["cpu_baseline"] = cb
+        if shared_gpu:
+            line["shared_gpu_functional_check"] = True  # N ranks on one GPU: timings are not a measurement
+        dump = os.environ.get("LTCI_BENCH_DUMP_PEAKS")
+        if dump and cpis == 1:
+            # the job's per-row peak map (R x {idx lo, idx hi, re, im}) after the rank
+            # merge of the last e2e step (collectives already done on every rank)
+            torch.cuda.synchronize(dev)
+            if ws == 1:
+                full = peaks.view(torch.int32)
+            elif shard == "coarse":
+                full = merged
+            else:
+                stride = R // ws + 1
+                full = torch.cat([gathered[r * stride:r * stride + (r + 1) * R // ws - r * R // ws]
+                                  for r in range(ws)])
+            np.save(dump, full.cpu().numpy())
         print(json.dumps(line))
     if ws > 1:
         dist.destroy_process_group()
