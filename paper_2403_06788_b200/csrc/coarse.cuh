@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT
     {
         constexpr int S = K / 16;
         const int total = PG * S;
-#pragma unroll 1
         constexpr int H = OUT16 ? 2 : 1;  // butterflies in flight per thread (register budget)
+#pragma unroll 1
         for (int i0 = tid; i0 < total; i0 += H * NT) {
             float2 v[H][16];
 #pragma unroll
