@@ -62,8 +62,14 @@ constexpr int kCoarseThreads = 512;      // fp16-output (tcgen05 path) CTAs and 
 constexpr int kCoarseSamples = 16384;
 template <int OUT16>
 __host__ __device__ constexpr int coarse_threads() { return OUT16 ? kCoarseThreads : 256; }
+#ifndef LTCI_COARSE_MINB32
+#define LTCI_COARSE_MINB32 3  // fp32-output CTAs per SM (register cap 65536 / (256 x this))
+#endif
+#ifndef LTCI_COARSE_H32
+#define LTCI_COARSE_H32 1  // fp32 output: pass-1 butterflies in flight per thread
+#endif
 template <int OUT16>
-__host__ __device__ constexpr int coarse_min_blocks() { return OUT16 ? 1 : 3; }
+__host__ __device__ constexpr int coarse_min_blocks() { return OUT16 ? 1 : LTCI_COARSE_MINB32; }
 __host__ __device__ constexpr int coarse_samples(int out16) { return out16 ? kCoarseSamples : 8192; }
 
 __host__ __device__ constexpr int coarse_pg_for(int K, int M, int out16 = 1) {
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT
     {
         constexpr int S = K / 16;
         const int total = PG * S;
-        constexpr int H = OUT16 ? 2 : 1;  // butterflies in flight per thread (register budget)
+        constexpr int H = OUT16 ? 2 : LTCI_COARSE_H32;  // butterflies in flight per thread (register budget)
 #pragma unroll 1
         for (int i0 = tid; i0 < total; i0 += H * NT) {
             float2 v[H][16];
