@@ -150,8 +150,26 @@ void build_fine_tables(Plan& pl) {
         // range-cell shards still reproduce the 1-GPU map bit for bit
         const double warps = static_cast<double>(pl.coarse_cells) * pl.R_total * M / 1024.0;
         const double want = 148.0 * 16.0 * 3.0;
-        int ns = static_cast<int>(std::ceil(want / std::max(1.0, warps)));
-        ns = std::max(1, std::min(ns, pl.n_inner / 16));
+        int ns = 1;
+        if (warps < want) {
+            // under ~3 waves: pick the split with the smallest wave-quantised makespan,
+            // waves x (chunk + 2) fine cells (2 ~ the per-CTA row load and seeding);
+            // 8-warp CTAs of 8 x 32/G rows, 2 per SM (fine_fft_tm_kernel launch bounds)
+            const long long rows_per_cta = 8LL * (32 / (M / 32));
+            const long long ctas = (static_cast<long long>(pl.coarse_cells) * pl.R_total + rows_per_cta - 1) /
+                                   rows_per_cta;
+            const long long slots = 148LL * 2;
+            long long best = -1;
+            for (int cand = 1; cand <= std::max(1, pl.n_inner / 16); ++cand) {
+                const int ch = (pl.n_inner + cand - 1) / cand;
+                const int nsp = (pl.n_inner + ch - 1) / ch;
+                const long long cost = (ctas * nsp + slots - 1) / slots * (ch + 2);
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    ns = cand;
+                }
+            }
+        }
         if (ns > 1) {
             pl.chunk = (pl.n_inner + ns - 1) / ns;
             pl.n_split = (pl.n_inner + pl.chunk - 1) / pl.chunk;
