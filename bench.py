@@ -56,6 +56,7 @@ def parse():
                     help="per-cell false-alarm rate of the retention threshold; 0 = min(1e-6, 1e5 / hypotheses), "
                          "i.e. 1e-6 unless that would retain more than ~1e5 noise cells per CPI (C2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lanes", type=int, default=2, help="engine lanes for a CPI stream (configs[4])")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample length")
     ap.add_argument("--coarse-slice", type=int, default=0,
                     help="restrict the coarse-velocity axis (rate measurement of configs too large for one step)")
@@ -319,6 +320,11 @@ def main():
         my_cpis = [0]
     log("engine")
     eng = Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi, coarse_begin=c_lo, coarse_end=c_hi)
+    # a CPI stream runs on two engine lanes (own buffers and stream each), so one
+    # CPI's last fine wave overlaps the next CPI's coarse stage and first waves
+    n_lanes = 2 if len(my_cpis) > 1 and args.lanes > 1 else 1
+    lane_engs = [eng] + [Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi, coarse_begin=c_lo,
+                                coarse_end=c_hi) for _ in range(n_lanes - 1)]
     log("synthesising cubes")
     hyp, integ = eng.work()
 
@@ -352,11 +358,27 @@ def main():
             pad[:n_rows].copy_(peaks.view(torch.int32))
             all_gather_into(gathered, pad)
 
+    lane_streams = [stream] + [torch.cuda.Stream(dev) for _ in range(n_lanes - 1)]
+    lane_peaks = [peaks] + [torch.as_tensor(_CAI(e.peaks_device()[0], (n_rows, 4), "<u4"), device=dev)
+                            for e in lane_engs[1:]]
+
     def step_local():
+        if n_lanes == 1:
+            for i, dc in enumerate(d_cubes):
+                eng.run_device(dc.data_ptr(), sptr)
+                if cpis > 1:
+                    per_cpi_peaks[i].copy_(peaks.view(torch.int32))  # keep each CPI's peak map
+            return
+        for ls in lane_streams[1:]:
+            ls.wait_stream(stream)
         for i, dc in enumerate(d_cubes):
-            eng.run_device(dc.data_ptr(), sptr)
-            if cpis > 1:
-                per_cpi_peaks[i].copy_(peaks.view(torch.int32))  # keep each CPI's peak map
+            ln = i % n_lanes
+            ls = lane_streams[ln]
+            lane_engs[ln].run_device(dc.data_ptr(), ls.cuda_stream)
+            with torch.cuda.stream(ls):
+                per_cpi_peaks[i].copy_(lane_peaks[ln].view(torch.int32))
+        for ls in lane_streams[1:]:
+            stream.wait_stream(ls)
 
     def step():
         step_local()
@@ -420,10 +442,19 @@ def main():
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         d2h = 0
-        for hst in hosts:
-            eng.run_host_ptr(hst.data_ptr(), sptr)
-            m = eng.result(sptr)
-            d2h += 8 + 16 * n_rows + 16 * int(m.cand_index.size)
+        pending = [None] * n_lanes  # two-deep pipeline over the lanes: CPI i+1 uploads and runs while i drains
+        for k, hst in enumerate(hosts):
+            ln = k % n_lanes
+            ls = lane_streams[ln].cuda_stream
+            if pending[ln] is not None:
+                m = lane_engs[ln].result(ls)
+                d2h += 8 + 16 * n_rows + 16 * int(m.cand_index.size)
+            lane_engs[ln].run_host_ptr(hst.data_ptr(), ls)
+            pending[ln] = k
+        for ln in range(n_lanes):
+            if pending[ln] is not None:
+                m = lane_engs[ln].result(lane_streams[ln].cuda_stream)
+                d2h += 8 + 16 * n_rows + 16 * int(m.cand_index.size)
         if ws > 1:
             gather_peaks()
             torch.cuda.synchronize(dev)
@@ -554,7 +585,8 @@ def main():
         print(json.dumps(line))
     if ws > 1:
         dist.destroy_process_group()
-    eng.close()
+    for e in lane_engs:
+        e.close()
 
 
 if __name__ == "__main__":
