@@ -60,8 +60,11 @@ struct CoarseArgs {
 // shards reproduce the 1-GPU map bit for bit).
 constexpr int kCoarseThreads = 512;      // fp16-output (tcgen05 path) CTAs and fd_grft
 constexpr int kCoarseSamples = 16384;
+#ifndef LTCI_COARSE_NT32
+#define LTCI_COARSE_NT32 256  // fp32-output CTA size
+#endif
 template <int OUT16>
-__host__ __device__ constexpr int coarse_threads() { return OUT16 ? kCoarseThreads : 256; }
+__host__ __device__ constexpr int coarse_threads() { return OUT16 ? kCoarseThreads : LTCI_COARSE_NT32; }
 #ifndef LTCI_COARSE_MINB32
 #define LTCI_COARSE_MINB32 3  // fp32-output CTAs per SM (register cap 65536 / (256 x this))
 #endif
