@@ -541,7 +541,7 @@ def main():
         line = {
             "metric": metric, "value": val, "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,  # the same job at every N, split across ranks
             "dtype": "c64 / fp32" if not use_tc else ("fp16x3 split (FP32 class)" if terms == 3 else "fp16"),
             "data": "synthetic (seeded reference signal model: CN(0,1) range noise + targets)",
             "config": {"workload": w.name, "config_index": args.config, "K": p.K, "M": p.M, "cpis": cpis,
