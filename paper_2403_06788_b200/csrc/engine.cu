@@ -1020,8 +1020,20 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
     const Plan& pl = e->pl;
     DeviceGuard dg(e->device);
     unsigned long long count = 0;
-    CK(cudaMemcpyAsync(&count, e->cand_count.p, sizeof(count), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    // the count, the per-row peak slots and the optional dense map come back
+    // behind one synchronisation (re-copied below in the rare re-run case)
+    std::vector<PeakSlot> slots(pl.R_slice);
+    std::vector<float2> dense;
+    auto fetch = [&] {
+        CK(cudaMemcpyAsync(&count, e->cand_count.p, sizeof(count), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(slots.data(), e->slots.p, slots.size() * sizeof(PeakSlot), cudaMemcpyDeviceToHost, st));
+        if (pl.keep_dense) {
+            dense.resize(static_cast<size_t>(pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D));  // not the (grow-only) buffer
+            CK(cudaMemcpyAsync(dense.data(), e->dense.p, dense.size() * sizeof(float2), cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
+    };
+    fetch();
     if (count > e->cand_cap) {
         // The reference would try to hold every retained cell in host memory
         // (24 B each); refuse what cannot fit rather than hang.
@@ -1036,8 +1048,7 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         e->cand_cap = count;
         e->cand.ensure(count);
         run_device_impl(e, e->last_cube, st);
-        CK(cudaMemcpyAsync(&count, e->cand_count.p, sizeof(count), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        fetch();
     }
 
     auto* out = static_cast<ltci_detection_map*>(std::calloc(1, sizeof(ltci_detection_map)));
@@ -1052,15 +1063,6 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         out->doppler_first = pl.dop_first;
 
         // peak slots -> per-row peaks + global argmax
-        std::vector<PeakSlot> slots(pl.R_slice);
-        CK(cudaMemcpyAsync(slots.data(), e->slots.p, slots.size() * sizeof(PeakSlot), cudaMemcpyDeviceToHost, st));
-        std::vector<float2> dense;
-        if (pl.keep_dense) {
-            dense.resize(static_cast<size_t>(pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D));  // not the (grow-only) buffer
-            CK(cudaMemcpyAsync(dense.data(), e->dense.p, dense.size() * sizeof(float2), cudaMemcpyDeviceToHost, st));
-        }
-        CK(cudaStreamSynchronize(st));
-
         out->n_rows = pl.R_slice;
         out->peak_index = static_cast<uint64_t*>(xmalloc(pl.R_slice * sizeof(uint64_t)));
         out->peak_value = static_cast<double*>(xmalloc(2 * pl.R_slice * sizeof(double)));
