@@ -232,9 +232,15 @@ class _CAI:
 
 
 def _ncu_traffic(config_index, kernel):
-    """DRAM bytes per launch of ``kernel`` from the committed ncu --set full capture (C1 only)."""
+    """DRAM bytes per launch of the fine kernel from the committed ncu --set full captures
+    (C1: ``kernel`` in profiles/r01_ncu_c1.json; other configs: profiles/r01_ncu_traffic.json)."""
+    if config_index != 1:
+        path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+        if kernel.startswith("fine_tc") or not os.path.exists(path):
+            return None
+        return json.load(open(path)).get(str(config_index), {}).get("traffic_bytes_per_launch")
     path = os.path.join(ROOT, "profiles", "r01_ncu_c1.json")
-    if config_index != 1 or not os.path.exists(path):
+    if not os.path.exists(path):
         return None
     return json.load(open(path)).get(kernel, {}).get("traffic_bytes_per_launch")
 
@@ -517,8 +523,11 @@ def main():
                     "kernel": kname,
                     "achieved": achieved, "peak": fp32.value, "unit": "TFLOP/s",
                     "frac": achieved / fp32.value if fp32.value else None,
-                    "traffic": _ncu_traffic(args.config, "fine_fft_tm_kernel<0>") if tm else None,
-                    "traffic_source": "profiles/r01_ncu_c1.json (ncu --set full, bytes per launch)",
+                    "traffic": _ncu_traffic(args.config, "fine_fft_tm_kernel<0>")
+                    if 256 <= p.M <= 2048 and (args.config != 2 or (args.coarse_slice == 1 and args.coarse_rest == 1))
+                    else None,
+                    "traffic_source": ("profiles/r01_ncu_c1.json" if args.config == 1 else "profiles/r01_ncu_traffic.json")
+                    + " (ncu --set full, DRAM bytes per launch)",
                     "peak_source": "measured in-run FFMA chain microbenchmark (ltci_cuda_measure_fp32_peak)",
                     "algorithmic": "per (row, fine cell): 6M chirp + 5M log2M FFT + 3D |Y|^2 flop",
                     "dense_equiv_tflops": 8.0 * integ / fine_s / 1e12}
