@@ -170,6 +170,7 @@ void build_fine_tables(Plan& pl) {
                 }
             }
         }
+        if (const char* env = std::getenv("LTCI_FINE_NSPLIT")) ns = std::max(1, std::atoi(env));  // A/B only
         if (ns > 1) {
             pl.chunk = (pl.n_inner + ns - 1) / ns;
             pl.n_split = (pl.n_inner + pl.chunk - 1) / pl.chunk;
