@@ -56,7 +56,7 @@ def parse():
                     help="per-cell false-alarm rate of the retention threshold; 0 = min(1e-6, 1e5 / hypotheses), "
                          "i.e. 1e-6 unless that would retain more than ~1e5 noise cells per CPI (C2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=2, help="engine lanes for a CPI stream (configs[4])")
+    ap.add_argument("--lanes", type=int, default=3, help="engine lanes for a CPI stream (configs[4])")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample length")
     ap.add_argument("--coarse-slice", type=int, default=0,
                     help="restrict the coarse-velocity axis (rate measurement of configs too large for one step)")
@@ -326,9 +326,9 @@ def main():
         my_cpis = [0]
     log("engine")
     eng = Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi, coarse_begin=c_lo, coarse_end=c_hi)
-    # a CPI stream runs on two engine lanes (own buffers and stream each), so one
+    # a CPI stream runs on --lanes engine lanes (own buffers and stream each), so one
     # CPI's last fine wave overlaps the next CPI's coarse stage and first waves
-    n_lanes = 2 if len(my_cpis) > 1 and args.lanes > 1 else 1
+    n_lanes = max(1, min(args.lanes, len(my_cpis)))
     lane_engs = [eng] + [Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi, coarse_begin=c_lo,
                                 coarse_end=c_hi) for _ in range(n_lanes - 1)]
     log("synthesising cubes")
@@ -448,7 +448,7 @@ def main():
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         d2h = 0
-        pending = [None] * n_lanes  # two-deep pipeline over the lanes: CPI i+1 uploads and runs while i drains
+        pending = [None] * n_lanes  # pipeline over the lanes: later CPIs upload and run while earlier ones drain
         for k, hst in enumerate(hosts):
             ln = k % n_lanes
             ls = lane_streams[ln].cuda_stream
