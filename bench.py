@@ -144,9 +144,54 @@ def fft_flops_per_row_cell(M: int, D: int) -> float:
     return 6.0 * M + 5.0 * M * math.log2(M) + 3.0 * D
 
 
-def cpu_reference_rate(w, seconds_target: float, threads: int):
+def metric_of(w):
+    """(metric, unit) of a workload -- ONE definition for both arms, so the
+    driver can divide them (BASELINE.json metric: G/s, CPIs/s for a stream)."""
+    name = "DS-GRFT" if w.variant == 0 else "DS-KT-MFP"
+    if w.cpis > 1:
+        return f"{name} CPIs/s ({w.cpis}-CPI stream)", "CPI/s"
+    return f"{name} motion-hypothesis x pulse integrations/s", "G/s"
+
+
+def in_unit(w, gps: float) -> float:
+    """A G/s rate in the workload's metric unit (CPI/s for a CPI stream)."""
+    return gps * 1e9 / w.integrations() if w.cpis > 1 else gps
+
+
+def n_coarse_cells(w) -> int:
+    s = w.space
+    return int(np.prod([g.count for g in s.coarse])) if w.variant == 0 else w.amb.count() * s.coarse[1].count
+
+
+def plan_shard(w, ws: int, requested: str) -> str:
+    """The job's partition across ``ws`` ranks (the same answer in both arms)."""
+    if w.cpis > 1:
+        return "cpis"
+    if requested == "auto":
+        return "coarse" if n_coarse_cells(w) >= ws else "rows"
+    return requested
+
+
+def job_config(w, args, ws: int) -> dict:
+    """``config`` of the JSON line: the workload and its partition, identical in both arms."""
+    p = w.params
+    shard = plan_shard(w, ws, args.shard)
+    return {"workload": w.name, "config_index": args.config, "K": p.K, "M": p.M, "cpis": w.cpis,
+            "hypotheses_per_cpi": w.hypotheses(), "integrations_per_step": w.integrations() * w.cpis,
+            "parallelism": {"cpis": "CPI shards", "coarse": "coarse-cell shards",
+                            "rows": "range-cell shards"}[shard] + f" x{ws}",
+            "l2": "GPU arm: flushed between steps (512 MiB write, untimed); X stream >> L2"}
+
+
+def cpu_reference_rate(w, seconds_target: float, threads: int, full=None):
     """Time the reference's own detector (oracle/_ref, compiled from the
-    reference sources) on a coarse-cell slice sized to ~seconds_target."""
+    reference sources) on a coarse-cell slice sized to ~seconds_target.
+    ``full``: the unsliced workload when ``w`` is itself a coarse slice, so the
+    sample can still give every host thread a coarse cell (every coarse cell
+    costs the same, so the per-integration rate is the slice's)."""
+    unit_w = w
+    if full is not None:
+        w = full
     import oracle as O
     from paper_2403_06788_b200 import configs, scene
     from paper_2403_06788_b200.model import DetectorOptions
@@ -191,36 +236,38 @@ def cpu_reference_rate(w, seconds_target: float, threads: int):
     cells = (sl.amb.count() * sl.space.coarse[1].count if sl.variant == 1
              else int(np.prod([g.count for g in sl.space.coarse])))
     used = max(1, min(threads, cells))
-    return {"value": integ / dt / 1e9, "unit": "G/s", "cores": used, "kind": "reference",
+    return {"value": in_unit(unit_w, integ / dt / 1e9), "unit": metric_of(unit_w)[1], "cores": used,
+            "kind": "reference",
             "sample": f"{sl.name}: {integ:.3e} integrations in {dt:.2f} s (oracle/_ref, -O3, threads={threads})"}
 
 
-def run_reference(args, w, ws, rank):
+def run_reference(args, w, ws, rank, w_full=None):
     if rank != 0:
         return
     import oracle as O
     threads = os.cpu_count() or 1
-    line = {"impl": "reference", "metric": "DS-GRFT integrations/s (hypothesis x pulse)", "unit": "G/s",
+    metric, unit = metric_of(w)
+    line = {"impl": "reference", "metric": metric, "unit": unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "config": {"workload": w.name, "config_index": args.config}, "data": "synthetic (seeded)"}
+            "config": job_config(w, args, ws), "data": "synthetic (seeded reference signal model)"}
     if not O.have_ref():
         line["unavailable"] = "reference library oracle/_ref/libltci_ref.so not built"
         print(json.dumps(line))
         return
     for _ in range(args.warmup):
-        cpu_reference_rate(w, args.cpu_seconds, threads)
+        cpu_reference_rate(w, args.cpu_seconds, threads, w_full)
     vals, samples = [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r = cpu_reference_rate(w, args.cpu_seconds, threads)
+        r = cpu_reference_rate(w, args.cpu_seconds, threads, w_full)
         vals.append(r["value"])
         samples.append(r["sample"])
     total = time.perf_counter() - t0
     v = float(np.mean(vals))
     line.update({"value": v, "ms_per_step": total / args.steps * 1e3, "dtype": "f64",
-                 "cpu_baseline": {"value": v, "unit": "G/s", "cores": threads, "kind": "reference",
+                 "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "reference",
                                   "sample": samples[-1]},
-                 "e2e": {"value": v, "unit": "G/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+                 "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     print(json.dumps(line))
 
 
@@ -249,11 +296,11 @@ def main():
     args = parse()
     ws, rank, local = dist_env()
     from paper_2403_06788_b200 import configs
-    w = configs.config(args.config)
+    w = w_full = configs.config(args.config)
     if args.coarse_slice:
         w = configs.sliced(w, args.coarse_slice, args.coarse_rest)
     if args.impl == "reference":
-        run_reference(args, w, ws, rank)
+        run_reference(args, w, ws, rank, w_full)
         return
 
     import torch
@@ -273,23 +320,13 @@ def main():
         if shared_gpu:
             dist.init_process_group("gloo")
         else:
+            # communicator lines (nRanks, transport) stay on stderr as the run's evidence
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    def all_gather_into(out, inp):
-        if not shared_gpu:
-            dist.all_gather_into_tensor(out, inp)
-            return
-        parts = [torch.empty_like(inp, device="cpu") for _ in range(ws)]
-        dist.all_gather(parts, inp.cpu())
-        out.copy_(torch.cat(parts).view_as(out))
-
-    def all_reduce_max(t):
-        if not shared_gpu:
-            all_reduce_max(t)
-            return
-        h = t.cpu()
-        dist.all_reduce(h, op=dist.ReduceOp.MAX)
-        t.copy_(h)
+    from paper_2403_06788_b200.parallel import PeakGather, RankComm
+    comm = RankComm(ws, host_staged=shared_gpu)
     dev = torch.device("cuda", local)
     p, s = w.params, w.space
     fine_path = {"auto": A.FINE_AUTO, "fft": A.FINE_FFT_CUDA_CORE, "tc": A.FINE_TC_DENSE,
@@ -304,15 +341,12 @@ def main():
         n_coarse = int(np.prod([g.count for g in s.coarse]))
     else:
         n_coarse = w.amb.count() * s.coarse[1].count
-    shard = args.shard
-    if shard == "auto":
-        shard = "coarse" if n_coarse >= ws else "rows"
+    shard = plan_shard(w, ws, args.shard)
     c_lo, c_hi = 0, -1
     if cpis > 1:
         # CPI-level data parallelism (configs[4]): each rank streams its CPIs, full ROI
         lo, hi = 0, R
         my_cpis = list(range(rank * cpis // ws, (rank + 1) * cpis // ws))
-        shard = "cpis"
     elif shard == "coarse":
         # one CPI sharded over coarse cells (SURVEY.md 8(e) alternative): every rank
         # searches its coarse cells over every ROI row, nothing replicated
@@ -344,25 +378,19 @@ def main():
     peaks = torch.as_tensor(_CAI(peak_ptr, (n_rows, 4), "<u4"), device=dev)
     per_cpi_peaks = torch.empty((len(my_cpis), n_rows, 4), dtype=torch.int32, device=dev)
     lib = _lib.load()
-    if ws > 1 and shard == "coarse":
-        gathered = torch.empty((ws, R, 4), dtype=torch.int32, device=dev)
-        merged = torch.empty((R, 4), dtype=torch.int32, device=dev)
-    elif ws > 1:
-        gathered = torch.empty((ws * (R // ws + 1), 4), dtype=torch.int32, device=dev)
-
-    def gather_peaks():
-        if ws > 1 and shard == "coarse":
-            # every rank holds a peak per row: NCCL all-gather of the 16-byte records,
-            # then the per-row max on the device with the kernels' tie-break
-            all_gather_into(gathered, peaks.view(torch.int32))
+    gather = None
+    if ws > 1 and cpis == 1:
+        def merge_on_device(gathered, merged):
             _lib.raise_for(lib.ltci_cuda_merge_peaks(ctypes.c_void_p(gathered.data_ptr()), ws, R,
                                                      ctypes.c_void_p(merged.data_ptr()), ctypes.c_void_p(sptr)),
                            lib)
-        elif ws > 1 and cpis == 1:
-            # slices differ by at most one row: pad to a common length
-            pad = torch.zeros((R // ws + 1, 4), dtype=torch.int32, device=dev)
-            pad[:n_rows].copy_(peaks.view(torch.int32))
-            all_gather_into(gathered, pad)
+        # coarse shards: NCCL all-gather of the 16-byte records, then the per-row max on
+        # the device with the kernels' tie-break; row shards: padded all-gather
+        gather = PeakGather(comm, shard, R, peaks, merge=merge_on_device)
+
+    def gather_peaks():
+        if gather is not None:
+            gather(peaks.view(torch.int32))
 
     lane_streams = [stream] + [torch.cuda.Stream(dev) for _ in range(n_lanes - 1)]
     lane_peaks = [peaks] + [torch.as_tensor(_CAI(e.peaks_device()[0], (n_rows, 4), "<u4"), device=dev)
@@ -424,7 +452,7 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
-        all_reduce_max(t)
+        comm.all_reduce_max(t)
     ms_max = float(t.item())
     total_integ = w.integrations() * cpis  # all ranks together cover every hypothesis of every CPI once
     value = total_integ * args.steps / (ms_max * 1e-3) / 1e9
@@ -469,7 +497,7 @@ def main():
             e2e_ms.append((t1 - t0) * 1e3)
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if ws > 1:
-        all_reduce_max(e2e_t)
+        comm.all_reduce_max(e2e_t)
     e2e_value = total_integ * args.steps / (float(e2e_t.item()) * 1e-3) / 1e9
 
     if rank == 0:
@@ -541,26 +569,21 @@ def main():
                                       "fp32_algorithmic": "per (coarse cell, pulse): 5 K log2 K FFT + 8 K ramp",
                                       "note": "exact fractional-delay gather = one K-point transform per "
                                               "(coarse cell, pulse); issue-bound, see profiles/r01_ncu_c1.json"}})
-        name = "DS-GRFT" if w.variant == 0 else "DS-KT-MFP"
+        metric, unit = metric_of(w)
         if cpis > 1:
-            metric, unit, val, e2e_val = f"{name} CPIs/s ({cpis}-CPI stream)", "CPI/s", cpi_rate, \
-                cpis * args.steps / (float(e2e_t.item()) * 1e-3)
+            val, e2e_val = cpi_rate, cpis * args.steps / (float(e2e_t.item()) * 1e-3)
         else:
-            metric, unit, val, e2e_val = f"{name} motion-hypothesis x pulse integrations/s", "G/s", value, e2e_value
+            val, e2e_val = value, e2e_value
         line = {
             "metric": metric, "value": val, "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,  # the same job at every N, split across ranks
             "dtype": "c64 / fp32" if not use_tc else ("fp16x3 split (FP32 class)" if terms == 3 else "fp16"),
             "data": "synthetic (seeded reference signal model: CN(0,1) range noise + targets)",
-            "config": {"workload": w.name, "config_index": args.config, "K": p.K, "M": p.M, "cpis": cpis,
-                       "hypotheses_per_cpi": w.hypotheses(), "integrations_per_step": total_integ,
-                       "integrations_per_s_G": value,
-                       "parallelism": {"cpis": "CPI shards", "coarse": "coarse-cell shards",
-                                       "rows": "range-cell shards"}[shard] + f" x{ws}",
-                       "retain_threshold": gamma, "pfa": args.pfa,
-                       "l2": "flushed between steps (512 MiB write, untimed); X stream >> L2",
-                       "fine_path": args.fine_path + (" -> tcgen05" if use_tc else " -> cuda-core fft")},
+            "config": job_config(w, args, ws),
+            "run": {"integrations_per_s_G": value, "retain_threshold": gamma, "pfa": args.pfa,
+                    "fine_path": args.fine_path + (" -> tcgen05" if use_tc else " -> cuda-core fft"),
+                    "lanes": n_lanes},
             "roofline": roof,
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": int(cube.size * 16 * len(cubes)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms))},
@@ -571,7 +594,7 @@ def main():
         if ws == 1 and not args.no_cpu_baseline:
             try:
                 log("cpu baseline")
-                cb = cpu_reference_rate(w, args.cpu_seconds, os.cpu_count() or 1)
+                cb = cpu_reference_rate(w, args.cpu_seconds, os.cpu_count() or 1, w_full)
             except Exception as e:  # reported, not fatal
                 cb = {"error": str(e)}
             line["cpu_baseline"] = cb
@@ -582,14 +605,7 @@ def main():
             # the job's per-row peak map (R x {idx lo, idx hi, re, im}) after the rank
             # merge of the last e2e step (collectives already done on every rank)
             torch.cuda.synchronize(dev)
-            if ws == 1:
-                full = peaks.view(torch.int32)
-            elif shard == "coarse":
-                full = merged
-            else:
-                stride = R // ws + 1
-                full = torch.cat([gathered[r * stride:r * stride + (r + 1) * R // ws - r * R // ws]
-                                  for r in range(ws)])
+            full = peaks.view(torch.int32) if ws == 1 else gather.full_map()
             np.save(dump, full.cpu().numpy())
         print(json.dumps(line))
     if ws > 1:

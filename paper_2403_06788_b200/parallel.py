@@ -238,3 +238,130 @@ def split_map_by_coarse(full: DetectionMap, C: int, world: int) -> List[Detectio
         m.cand_index, m.cand_value = full.cand_index[cs].copy(), full.cand_value[cs].copy()
         out.append(m)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Collectives of the N-rank bench path (bench.py).  One object, two transports:
+# device tensors over NCCL (the real path: one GPU per rank), or, when every
+# rank shares one GPU for a functional check (LTCI_BENCH_SHARED_GPU=1), host
+# copies over gloo.  Both branches run under gloo in tests/test_multi.py.
+
+class RankComm:
+    """``all_gather_into`` / ``all_reduce_max`` for the bench's peak records
+    and timings.  ``host_staged=False``: the tensors go to the collective as
+    they are (NCCL with device tensors, or gloo with host tensors);
+    ``host_staged=True``: device tensors are staged through host memory
+    (gloo cannot take them)."""
+
+    def __init__(self, world: int, host_staged: bool = False, group=None):
+        self.world = world
+        self.host_staged = host_staged
+        self.group = group
+
+    def all_gather_into(self, out, inp) -> None:
+        """``out`` (world x inp.numel(), rank-major) <- every rank's ``inp``."""
+        import torch
+        import torch.distributed as dist
+        if not self.host_staged:
+            # rank-major concatenation along dim 0 (gloo checks the shape, NCCL only numel)
+            dist.all_gather_into_tensor(out.view(-1, *inp.shape[1:]), inp, group=self.group)
+            return
+        parts = [torch.empty_like(inp, device="cpu") for _ in range(self.world)]
+        dist.all_gather(parts, inp.cpu(), group=self.group)
+        out.copy_(torch.cat(parts).view_as(out))
+
+    def all_reduce_max(self, t) -> None:
+        """Element-wise max over ranks, in place (the max-over-ranks timing)."""
+        import torch.distributed as dist
+        if not self.host_staged:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            return
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=self.group)
+        t.copy_(h)
+
+
+def _mag2f_np(re: np.ndarray, im: np.ndarray) -> np.ndarray:
+    """fmaf(re, re, im*im) in FP32, as ``mag2f`` (csrc/common.cuh) evaluates it:
+    re*re is exact in FP64, so one FP32 rounding of the FP64 sum matches the
+    fused form except at double-rounding boundaries."""
+    im2 = (im.astype(np.float32) * im.astype(np.float32)).astype(np.float32)
+    return (re.astype(np.float64) * re.astype(np.float64) + im2.astype(np.float64)).astype(np.float32)
+
+
+def merge_peak_records(gathered: np.ndarray) -> np.ndarray:
+    """Host mirror of ``merge_peaks_kernel`` (csrc/engine.cu): per row, the
+    best 16-byte slot {f32 re, f32 im, u64 flat index} over the ranks of a
+    coarse-cell partition -- magnitude first, lowest flat index on ties, empty
+    slots (index 2^64-1) lose -- the reference's total order
+    (proj/src/detectors.cpp:23-31, 34-50).  ``gathered``: (ranks, R, 4) int32."""
+    g = np.ascontiguousarray(gathered).view(np.uint32).reshape(gathered.shape[0], -1, 4)
+    re = g[..., 0].view(np.float32)
+    im = g[..., 1].view(np.float32)
+    idx = g[..., 2].astype(np.uint64) | (g[..., 3].astype(np.uint64) << np.uint64(32))
+    empty = idx == np.uint64(0xFFFFFFFFFFFFFFFF)
+    mag = np.where(empty, np.float32(-1.0), _mag2f_np(re, im))
+    R = g.shape[1]
+    rows = np.arange(R)
+    best = np.zeros(R, np.int64)
+    for k in range(1, g.shape[0]):
+        bm, bi = mag[best, rows], idx[best, rows]
+        better = ~empty[k] & ((mag[k] > bm) | ((mag[k] == bm) & (idx[k] < bi)))
+        best = np.where(better, k, best)
+    return g[best, rows].view(np.int32).copy()
+
+
+def encode_peak_records(index: np.ndarray, value: np.ndarray) -> np.ndarray:
+    """(R, 4) int32 slots {re, im, idx lo, idx hi} as the engine stores them."""
+    out = np.zeros((index.size, 4), np.uint32)
+    out[:, 0] = value.real.astype(np.float32).view(np.uint32)
+    out[:, 1] = value.imag.astype(np.float32).view(np.uint32)
+    out[:, 2] = (index.astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    out[:, 3] = (index.astype(np.uint64) >> np.uint64(32)).astype(np.uint32)
+    return out.view(np.int32)
+
+
+class PeakGather:
+    """The per-row peak exchange of one sharded CPI (bench.py's N-rank step).
+
+    * ``shard="coarse"``: every rank holds a slot for every row R; all-gather the
+      (R, 4) records into (world, R, 4) and reduce per row with ``merge``
+      (``ltci_cuda_merge_peaks`` on the device; ``merge_peak_records`` on the
+      host) into ``merged``.
+    * ``shard="rows"``: rank k holds rows ``shard_rows(R, world, k)``; slices
+      differ by at most one row, so each is padded to R // world + 1 records,
+      all-gathered, and ``full_map`` cuts the padding back out.
+    """
+
+    def __init__(self, comm: RankComm, shard: str, R: int, like, merge=None):
+        import torch
+        if shard not in ("coarse", "rows"):
+            raise ValueError("PeakGather: shard must be 'coarse' or 'rows'")
+        self.comm, self.shard, self.R, self.merge = comm, shard, R, merge
+        w = comm.world
+        kw = dict(dtype=torch.int32, device=like.device)
+        if shard == "coarse":
+            self.gathered = torch.empty((w, R, 4), **kw)
+            self.merged = torch.empty((R, 4), **kw)
+        else:
+            self.stride = R // w + 1
+            self.gathered = torch.empty((w * self.stride, 4), **kw)
+            self.pad = torch.zeros((self.stride, 4), **kw)
+
+    def __call__(self, local) -> None:
+        """``local``: this rank's (rows, 4) int32 peak slots."""
+        if self.shard == "coarse":
+            self.comm.all_gather_into(self.gathered, local)
+            self.merge(self.gathered, self.merged)
+        else:
+            self.pad[: local.shape[0]].copy_(local)
+            self.comm.all_gather_into(self.gathered, self.pad)
+
+    def full_map(self):
+        """(R, 4) slots of the whole job after the last call."""
+        import torch
+        if self.shard == "coarse":
+            return self.merged
+        w = self.comm.world
+        return torch.cat([self.gathered[k * self.stride: k * self.stride + (hi - lo)]
+                          for k, (lo, hi) in enumerate(shard_rows(self.R, w, k) for k in range(w))])

@@ -154,3 +154,67 @@ def test_gloo_gather_matches_single_rank(world):
         pr.join(timeout=180)
         assert pr.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+# ---- bench.py's own collectives (parallel.RankComm / PeakGather), both branches
+
+def _worker_bench_comm(rank, world, port, staged, shard, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p, s, full, C = _small_dense()
+        R = s.roi.count()
+        comm = parallel.RankComm(world, host_staged=staged)
+        # max-over-ranks timing, as bench.py reduces its event times
+        t = torch.tensor([10.0 + rank], dtype=torch.float64)
+        comm.all_reduce_max(t)
+        ok = float(t.item()) == 10.0 + world - 1
+
+        def merge(gathered, merged):
+            merged.copy_(torch.from_numpy(parallel.merge_peak_records(gathered.numpy())))
+
+        g = parallel.PeakGather(comm, shard, R, torch.zeros(1), merge=merge)
+        if shard == "coarse":
+            local = parallel.split_map_by_coarse(full, C, world)[rank]
+        else:
+            D = doppler_window(p, s)[1]
+            local = parallel.split_map_by_rows(full, R, D, world)[rank]
+        g(torch.from_numpy(parallel.encode_peak_records(local.peak_index, local.peak_value)))
+        got = g.full_map().numpy().view(np.uint32)
+        want = parallel.encode_peak_records(full.peak_index, full.peak_value).view(np.uint32)
+        ok = ok and np.array_equal(got, want)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("staged", [False, True])
+@pytest.mark.parametrize("shard", ["coarse", "rows"])
+def test_gloo_bench_collectives(staged, shard):
+    """bench.py's N>1 helpers on both transports (direct and host-staged):
+    max-over-ranks reduction and the peak exchange reproduce the single-rank map."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_bench_comm, args=(r, world, port, staged, shard, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=180)
+        assert pr.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    assert res == [(r, True) for r in range(world)]
+
+
+def test_merge_peak_records_tie_break():
+    """Host mirror of merge_peaks_kernel: magnitude first, lowest index on ties,
+    empty slots lose."""
+    E = np.uint64(0xFFFFFFFFFFFFFFFF)
+    a = parallel.encode_peak_records(np.array([5, 9, E, 3], np.uint64), np.array([1 + 0j, 2j, 0, 3], np.complex128))
+    b = parallel.encode_peak_records(np.array([4, 8, 7, E], np.uint64), np.array([1j, 2 + 0j, 1e-3, 0], np.complex128))
+    m = parallel.merge_peak_records(np.stack([a, b])).view(np.uint32)
+    idx = m[:, 2].astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
+    assert idx.tolist() == [4, 8, 7, 3]
