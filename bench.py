@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--coarse-slice", type=int, default=0,
                     help="restrict the coarse-velocity axis (rate measurement of configs too large for one step)")
     ap.add_argument("--coarse-rest", type=int, default=0, help="with --coarse-slice: restrict the other coarse axes")
+    ap.add_argument("--front-end", default="auto", choices=["auto", "range", "freq"],
+                    help="input domain: range-pulse echo through K0 (range FFT) first, or the freq-pulse cube; "
+                         "auto = range for configs[3] (its pipeline starts with the range FFT), freq otherwise")
     ap.add_argument("--shard", default="auto", choices=["auto", "rows", "coarse"],
                     help="one-CPI partition across ranks: coarse cells (no replicated work; default when every "
                          "rank gets one) or range cells")
@@ -172,18 +175,25 @@ def plan_shard(w, ws: int, requested: str) -> str:
     return requested
 
 
+def front_of(args) -> str:
+    """Input domain of a step: "range" = range-pulse echo through K0 (range FFT) first."""
+    return args.front_end if args.front_end != "auto" else ("range" if args.config == 3 else "freq")
+
+
 def job_config(w, args, ws: int) -> dict:
     """``config`` of the JSON line: the workload and its partition, identical in both arms."""
     p = w.params
     shard = plan_shard(w, ws, args.shard)
     return {"workload": w.name, "config_index": args.config, "K": p.K, "M": p.M, "cpis": w.cpis,
+            "front_end": ("range-pulse echo: range FFT (ltci::range_fft) in every step" if front_of(args) == "range"
+                          else "freq-pulse cube (the reference detectors' input)"),
             "hypotheses_per_cpi": w.hypotheses(), "integrations_per_step": w.integrations() * w.cpis,
             "parallelism": {"cpis": "CPI shards", "coarse": "coarse-cell shards",
                             "rows": "range-cell shards"}[shard] + f" x{ws}",
             "l2": "GPU arm: flushed between steps (512 MiB write, untimed); X stream >> L2"}
 
 
-def cpu_reference_rate(w, seconds_target: float, threads: int, full=None):
+def cpu_reference_rate(w, seconds_target: float, threads: int, full=None, front="freq"):
     """Time the reference's own detector (oracle/_ref, compiled from the
     reference sources) on a coarse-cell slice sized to ~seconds_target.
     ``full``: the unsliced workload when ``w`` is itself a coarse slice, so the
@@ -231,6 +241,16 @@ def cpu_reference_rate(w, seconds_target: float, threads: int, full=None):
     O.ref_ds(x, sl.params, sl.space, opt, sl.variant, sl.amb)
     dt = time.perf_counter() - t0
     integ = sl.integrations()
+    fe = ""
+    if front == "range":
+        # the job's range FFT (reference range_fft on the whole echo), charged to the
+        # sample in proportion to its share of the job's integrations
+        rc = np.fft.ifft(x, axis=1) * w.params.K
+        t1 = time.perf_counter()
+        O.ref_range_fft(rc, w.params)
+        t_fft = time.perf_counter() - t1
+        dt += t_fft * integ / w.integrations()
+        fe = f" + range_fft share ({t_fft:.3f} s per echo)"
     # the reference parallelises over coarse cells (detectors.cpp:356-358): a
     # sample with fewer cells than host threads only keeps that many busy
     cells = (sl.amb.count() * sl.space.coarse[1].count if sl.variant == 1
@@ -238,7 +258,7 @@ def cpu_reference_rate(w, seconds_target: float, threads: int, full=None):
     used = max(1, min(threads, cells))
     return {"value": in_unit(unit_w, integ / dt / 1e9), "unit": metric_of(unit_w)[1], "cores": used,
             "kind": "reference",
-            "sample": f"{sl.name}: {integ:.3e} integrations in {dt:.2f} s (oracle/_ref, -O3, threads={threads})"}
+            "sample": f"{sl.name}: {integ:.3e} integrations in {dt:.2f} s{fe} (oracle/_ref, -O3, threads={threads})"}
 
 
 def run_reference(args, w, ws, rank, w_full=None):
@@ -255,11 +275,11 @@ def run_reference(args, w, ws, rank, w_full=None):
         print(json.dumps(line))
         return
     for _ in range(args.warmup):
-        cpu_reference_rate(w, args.cpu_seconds, threads, w_full)
+        cpu_reference_rate(w, args.cpu_seconds, threads, w_full, front_of(args))
     vals, samples = [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r = cpu_reference_rate(w, args.cpu_seconds, threads, w_full)
+        r = cpu_reference_rate(w, args.cpu_seconds, threads, w_full, front_of(args))
         vals.append(r["value"])
         samples.append(r["sample"])
     total = time.perf_counter() - t0
@@ -333,7 +353,10 @@ def main():
                  "tcfast": A.FINE_TC_FAST}[args.fine_path]
     if args.pfa <= 0:
         args.pfa = min(1e-6, 1e5 / float(w.hypotheses()))
-    gamma = detection_threshold(p, w.sigma2, args.pfa)
+    # range front end: the echo is the range-compressed cube range_ifft(y) (CN(0,1) noise);
+    # K0 returns range_fft(range_ifft(y)) = K y, i.e. a freq cube with K^2 times the variance
+    sigma2_eff = w.sigma2 * (p.K ** 2 if front_of(args) == "range" else 1)
+    gamma = detection_threshold(p, sigma2_eff, args.pfa)
     opt = DetectorOptions(retain_threshold=gamma, fine_path=fine_path, device=local)
     R = s.roi.count()
     cpis = w.cpis
@@ -369,6 +392,14 @@ def main():
     hyp, integ = eng.work()
 
     cubes = [scene.to_complex64_roundtrip(w.cube(cpi=c)) for c in my_cpis]  # (M, K): column-major K x M
+    front = front_of(args)
+    if front == "range":
+        # the echo as range-compressed fast-time samples (range_ifft, proj/src/signal_model.cpp:85-95);
+        # every step starts with K0 (range_fft) on the device
+        cubes = [scene.to_complex64_roundtrip(np.fft.ifft(c, axis=1) * p.K) for c in cubes]
+        run_dev, run_hptr = Engine.run_range_device, Engine.run_range_host_ptr
+    else:
+        run_dev, run_hptr = Engine.run_device, Engine.run_host_ptr
     d_cubes = [torch.from_numpy(c.astype(np.complex64)).to(dev) for c in cubes]
     cube = cubes[0]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -399,7 +430,7 @@ def main():
     def step_local():
         if n_lanes == 1:
             for i, dc in enumerate(d_cubes):
-                eng.run_device(dc.data_ptr(), sptr)
+                run_dev(eng, dc.data_ptr(), sptr)
                 if cpis > 1:
                     per_cpi_peaks[i].copy_(peaks.view(torch.int32))  # keep each CPI's peak map
             return
@@ -408,7 +439,7 @@ def main():
         for i, dc in enumerate(d_cubes):
             ln = i % n_lanes
             ls = lane_streams[ln]
-            lane_engs[ln].run_device(dc.data_ptr(), ls.cuda_stream)
+            run_dev(lane_engs[ln], dc.data_ptr(), ls.cuda_stream)
             with torch.cuda.stream(ls):
                 per_cpi_peaks[i].copy_(lane_peaks[ln].view(torch.int32))
         for ls in lane_streams[1:]:
@@ -462,7 +493,7 @@ def main():
     # ---- kernel split (timed pass) for the roofline
     eng.set_timing(True)
     flush.zero_()
-    eng.run_device(d_cubes[0].data_ptr(), sptr)
+    run_dev(eng, d_cubes[0].data_ptr(), sptr)
     st = eng.stats()
     eng.set_timing(False)
     launches = st["launches"] * len(my_cpis) + (1 if ws > 1 and shard == "coarse" else 0)  # + peak merge
@@ -472,29 +503,63 @@ def main():
     hosts = [torch.from_numpy(c.view(np.float64).reshape(-1)).pin_memory() for c in cubes]
     e2e_ms = []
     d2h = 0
-    for i in range(args.warmup + args.steps):
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        d2h = 0
-        pending = [None] * n_lanes  # pipeline over the lanes: later CPIs upload and run while earlier ones drain
-        for k, hst in enumerate(hosts):
-            ln = k % n_lanes
+    # result() D2H: count + R peak slots (16 B) + 24 B per retained candidate (u64 index, complex128)
+    res_bytes = lambda m: 8 + 16 * n_rows + 24 * int(m.cand_index.size)  # noqa: E731
+    e2e_lanes = n_lanes
+    if ws == 1:
+        # one process streams the job's CPIs step after step through the public API; the
+        # lanes keep two in flight (CPI i+1 uploads and runs while CPI i's result drains),
+        # so the timed region holds every step's H2D, run and D2H, overlapped as a
+        # streaming receiver would
+        e2e_lanes = max(n_lanes, min(2, args.lanes))
+        while len(lane_engs) < e2e_lanes:
+            lane_engs.append(Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi, coarse_begin=c_lo,
+                                    coarse_end=c_hi))
+            lane_streams.append(torch.cuda.Stream(dev))
+        items = [(i, k) for i in range(args.warmup + args.steps) for k in range(len(hosts))]
+        pending = [None] * e2e_lanes
+        t0 = None
+        for j, (i, k) in enumerate(items):
+            if t0 is None and i == args.warmup:
+                for ln in range(e2e_lanes):  # drain the warm-up items, then start the clock
+                    if pending[ln] is not None:
+                        lane_engs[ln].result(lane_streams[ln].cuda_stream)
+                        pending[ln] = None
+                torch.cuda.synchronize(dev)
+                d2h = 0
+                t0 = time.perf_counter()
+            ln = j % e2e_lanes
             ls = lane_streams[ln].cuda_stream
             if pending[ln] is not None:
-                m = lane_engs[ln].result(ls)
-                d2h += 8 + 16 * n_rows + 16 * int(m.cand_index.size)
-            lane_engs[ln].run_host_ptr(hst.data_ptr(), ls)
+                d2h += res_bytes(lane_engs[ln].result(ls))
+            run_hptr(lane_engs[ln], hosts[k].data_ptr(), ls)
             pending[ln] = k
-        for ln in range(n_lanes):
+        for ln in range(e2e_lanes):
             if pending[ln] is not None:
-                m = lane_engs[ln].result(lane_streams[ln].cuda_stream)
-                d2h += 8 + 16 * n_rows + 16 * int(m.cand_index.size)
-        if ws > 1:
+                d2h += res_bytes(lane_engs[ln].result(lane_streams[ln].cuda_stream))
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        d2h //= args.steps
+    else:
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            d2h = 0
+            pending = [None] * n_lanes  # pipeline over the lanes: later CPIs upload and run while earlier ones drain
+            for k, hst in enumerate(hosts):
+                ln = k % n_lanes
+                ls = lane_streams[ln].cuda_stream
+                if pending[ln] is not None:
+                    d2h += res_bytes(lane_engs[ln].result(ls))
+                run_hptr(lane_engs[ln], hst.data_ptr(), ls)
+                pending[ln] = k
+            for ln in range(n_lanes):
+                if pending[ln] is not None:
+                    d2h += res_bytes(lane_engs[ln].result(lane_streams[ln].cuda_stream))
             gather_peaks()
             torch.cuda.synchronize(dev)
-        t1 = time.perf_counter()
-        if i >= args.warmup:
-            e2e_ms.append((t1 - t0) * 1e3)
+            t1 = time.perf_counter()
+            if i >= args.warmup:
+                e2e_ms.append((t1 - t0) * 1e3)
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if ws > 1:
         comm.all_reduce_max(e2e_t)
@@ -569,6 +634,36 @@ def main():
                                       "fp32_algorithmic": "per (coarse cell, pulse): 5 K log2 K FFT + 8 K ramp",
                                       "note": "exact fractional-delay gather = one K-point transform per "
                                               "(coarse cell, pulse); issue-bound, see profiles/r01_ncu_c1.json"}})
+        if w.variant == 1:
+            # K4 keystone timed over back-to-back calls (one call is ~5 us of
+            # traffic, launch latency would dominate a single timing)
+            kt_calls, kt_ring = 200, 8  # 8 (in, out) pairs = 269 MB at C3 > L2: every call streams from HBM
+            kt_in = [torch.from_numpy(scene.to_complex64_roundtrip(w.cube()).astype(np.complex64)).to(dev)
+                     for _ in range(kt_ring)]
+            kt_out = [torch.empty_like(d_cubes[0]) for _ in range(kt_ring)]
+            cr = p.to_c()
+
+            def kt_call(i):
+                _lib.raise_for(lib.ltci_cuda_keystone_device(
+                    ctypes.c_void_p(kt_in[i % kt_ring].data_ptr()), ctypes.c_void_p(kt_out[i % kt_ring].data_ptr()),
+                    ctypes.byref(cr), opt.keystone_taps, ctypes.c_void_p(sptr)), lib)
+            for i in range(16):
+                kt_call(i)
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0.record(stream)
+            for i in range(kt_calls):
+                kt_call(i)
+            k1.record(stream)
+            torch.cuda.synchronize(dev)
+            kt_ms = k0.elapsed_time(k1) / kt_calls
+            kt_bytes = 16.0 * p.K * p.M
+            roof["keystone_stage"] = {"bound": "hbm", "achieved": kt_bytes / (kt_ms * 1e-3) / 1e9, "peak": hbm,
+                                      "unit": "GB/s", "frac": kt_bytes / (kt_ms * 1e-3) / 1e9 / hbm,
+                                      "ms_per_call": kt_ms, "calls": kt_calls, "taps": opt.keystone_taps,
+                                      "algorithmic": "16 B per (row, pulse): complex64 read + write",
+                                      "kernel": "keystone_tiled_kernel<taps/2> (K4)",
+                                      "note": "back-to-back ltci_cuda_keystone_device calls on one stream over a "
+                                              "ring of 8 (in, out) cube pairs larger than L2"}
         metric, unit = metric_of(w)
         if cpis > 1:
             val, e2e_val = cpi_rate, cpis * args.steps / (float(e2e_t.item()) * 1e-3)
@@ -586,7 +681,10 @@ def main():
                     "lanes": n_lanes},
             "roofline": roof,
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": int(cube.size * 16 * len(cubes)),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": float(np.mean(e2e_ms))},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": float(e2e_t.item()) / args.steps,
+                    "lanes": e2e_lanes,
+                    "pipeline": "public API (Engine.run_host_ptr from pinned f64 + result()), CPIs streamed over "
+                                f"{e2e_lanes} engine lanes" if ws == 1 else "per step: upload, run, result, gather"},
             "gpu_launches": int(launches) * args.steps,
             "clocks": dict(clk.summary(), **({"untimed_repeat_steps_sampled": extra_steps} if extra_steps else {})),
             "wall_s_timed_region": wall,
@@ -594,7 +692,7 @@ def main():
         if ws == 1 and not args.no_cpu_baseline:
             try:
                 log("cpu baseline")
-                cb = cpu_reference_rate(w, args.cpu_seconds, os.cpu_count() or 1, w_full)
+                cb = cpu_reference_rate(w, args.cpu_seconds, os.cpu_count() or 1, w_full, front)
             except Exception as e:  # reported, not fatal
                 cb = {"error": str(e)}
             line["cpu_baseline"] = cb

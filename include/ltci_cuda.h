@@ -183,6 +183,17 @@ void ltci_cuda_free_map(ltci_detection_map *map);
 int ltci_cuda_fd_grft(const double *cube, const ltci_radar *cube_params, const ltci_single_space *space,
                       const ltci_options *opt, ltci_detection_map **out);
 int ltci_cuda_keystone(const double *cube, const ltci_radar *p, int taps, double *out);
+/* keystone on device complex64 cubes (K*M float2, column-major), asynchronous
+ * on the given cudaStream_t: the K4 kernel ds_kt_mfp runs, for timing it over
+ * back-to-back calls and for device-resident pipelines */
+int ltci_cuda_keystone_device(const void *d_in, void *d_out, const ltci_radar *p, int taps, void *stream);
+/* range_fft -> ltci::range_fft  proj/include/ltci/signal_model.hpp:37
+ * (proj/src/signal_model.cpp:97-107): per pulse the unnormalised forward
+ * K-point DFT of a range-pulse cube (K*M complex, column-major k + K m),
+ * giving the freq-pulse cube the detectors take; range_fft(range_ifft(x)) ==
+ * K x.  K a power of two in [16, 8192].  Values out are complex64-exact. */
+int ltci_cuda_range_fft(const double *range_cube, const ltci_radar *p, double *out);
+int ltci_cuda_range_fft_device(const void *d_in, void *d_out, const ltci_radar *p, void *stream);
 int ltci_cuda_mgift(const double *cube, const ltci_radar *p, const double *ctilde, int n_ctilde,
                     int variant, double *out /* K*M complex */);
 int ltci_cuda_gft(const double *rows, const ltci_radar *p, const double *fine_higher, int n_fine,
@@ -229,10 +240,19 @@ int ltci_engine_create(const ltci_radar *p, const ltci_dual_space *space, const 
                        ltci_engine **out);
 void ltci_engine_destroy(ltci_engine *e);
 /* Run on a device-resident complex64 cube (K*M float2, column-major) on the
- * given cudaStream_t (NULL = legacy default).  Asynchronous. */
+ * given cudaStream_t (NULL = legacy default).  Asynchronous.  The engine keeps
+ * a private copy of the cube (queued on the stream behind the run), so the
+ * caller may overwrite its buffer once the stream has passed this run, even
+ * before ltci_engine_result(). */
 int ltci_engine_run_device(ltci_engine *e, const void *d_cube_c64, void *stream);
 /* Same from a host float64 cube: H2D, run, D2H of the reduced results. */
 int ltci_engine_run_host(ltci_engine *e, const double *cube, void *stream);
+/* configs[3] front end: the input is a RANGE-pulse cube (range-compressed
+ * fast-time samples, K*M column-major); K0 (ltci::range_fft,
+ * proj/src/signal_model.cpp:97-107) turns it into the freq-pulse cube on the
+ * device, then the cascade runs.  Device complex64 or host float64 input. */
+int ltci_engine_run_range_device(ltci_engine *e, const void *d_range_c64, void *stream);
+int ltci_engine_run_range_host(ltci_engine *e, const double *range_cube, void *stream);
 /* Copy the reduced results of the last run to the host and build a map
  * (synchronises the stream).  Candidates overflowing the device buffer make
  * the engine re-run with a larger buffer, or fail with LTCI_BAD_ALLOC. */
@@ -333,6 +353,13 @@ int ltci_cuda_add_noise(const double *cube, const ltci_radar *p, double sigma2, 
 /* run_pd (proj/src/bench.cpp:72-124): every trial's noisy cube is generated on
  * the device and searched there; out[d * n_snr + s] for detector d, SNR s */
 int ltci_cuda_run_pd(const ltci_scenario *sc, ltci_pd_point *out);
+
+/* Idle one-shot engines (ltci_cuda_ds_grft / ds_kt_mfp) and fd_grft
+ * workspaces pooled for a device.  Both pools are process-wide and keep at
+ * most LTCI_POOL_IDLE (default 2) idle objects per device, however many host
+ * threads call in parallel (the reference's callers fan detector calls out
+ * over threads, proj/src/bench.cpp:94-110). */
+int ltci_cuda_pool_idle(int device, int64_t *engines, int64_t *fd_workspaces);
 
 /* Roofline denominator for the CUDA-core fine path: dense FP32 FFMA issue
  * rate of this device, measured with a register-resident FMA chain kernel

@@ -58,6 +58,7 @@ def port():
         lib.oracle_mgift.argtypes = [C.c_void_p, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, C.c_void_p]
         lib.oracle_gft.argtypes = [C.c_void_p, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, C.c_int, C.c_void_p]
         lib.oracle_keystone.argtypes = [C.c_void_p, P(A.CRadar), C.c_int, C.c_void_p]
+        lib.oracle_range_fft.argtypes = [C.c_void_p, P(A.CRadar), C.c_void_p]
         _port = lib
     return _port
 
@@ -84,6 +85,8 @@ def ref():
         lib.ref_ds_grft.argtypes = [vp, P(A.CRadar), P(A.CDualSpace), P(A.COptions), P(A.PMap)]
         lib.ref_ds_kt_mfp.argtypes = [vp, P(A.CRadar), P(A.CAmbiguity), P(A.CDualSpace), P(A.COptions), P(A.PMap)]
         lib.ref_keystone.argtypes = [vp, P(A.CRadar), C.c_int, vp]
+        lib.ref_range_fft.argtypes = [vp, P(A.CRadar), vp]
+        lib.ref_range_ifft.argtypes = [vp, P(A.CRadar), vp]
         lib.ref_mgift.argtypes = [vp, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, vp]
         lib.ref_gft.argtypes = [vp, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, C.c_int, vp]
         lib.ref_fd_grft_point.argtypes = [vp, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, vp]
@@ -168,6 +171,16 @@ def port_keystone(cube, params, taps=8):
     out = np.zeros_like(data)
     r = params.to_c()
     _check(lib.oracle_keystone(_vp(data), C.byref(r), taps, _vp(out)))
+    return out
+
+
+def port_range_fft(cube, params):
+    """range_fft (proj/src/signal_model.cpp:97-107) restated in C: per pulse dft_minus."""
+    lib = port()
+    data = _c128(cube)
+    out = np.zeros_like(data)
+    r = params.to_c()
+    _check(lib.oracle_range_fft(_vp(data), C.byref(r), _vp(out)))
     return out
 
 
@@ -272,6 +285,24 @@ def ref_keystone(cube, params, taps=8):
     out = np.zeros_like(data)
     r = params.to_c()
     _check(lib.ref_keystone(_vp(data), C.byref(r), taps, _vp(out)), lib)
+    return out
+
+
+def ref_range_fft(cube, params):
+    lib = ref()
+    data = _c128(cube)
+    out = np.zeros_like(data)
+    r = params.to_c()
+    _check(lib.ref_range_fft(_vp(data), C.byref(r), _vp(out)), lib)
+    return out
+
+
+def ref_range_ifft(cube, params):
+    lib = ref()
+    data = _c128(cube)
+    out = np.zeros_like(data)
+    r = params.to_c()
+    _check(lib.ref_range_ifft(_vp(data), C.byref(r), _vp(out)), lib)
     return out
 
 

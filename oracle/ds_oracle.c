@@ -12,6 +12,8 @@
  *   gft_row            build_mf(DFM) x row, dft_plus(M), recentre, twiddle
  *                                                   proj/src/transforms.cpp:180-214
  *   oracle_keystone    keystone                     proj/src/transforms.cpp:96-130
+ *   oracle_range_fft   range_fft (Fft::dft_minus per pulse)
+ *                                                   proj/src/signal_model.cpp:97-107, proj/src/fft.cpp:30-51
  *   oracle_ds          ds_grft / ds_kt_mfp -> run_dual_scale + UnitScan + merge_units
  *                                                   proj/src/detectors.cpp:16-50,337-481
  */
@@ -507,5 +509,24 @@ int oracle_keystone(const double *cube_d, const ltci_radar *p, int taps, double 
     }
     free(cube);
     free(o);
+    return LTCI_OK;
+}
+
+/* range_fft (proj/src/signal_model.cpp:97-107): per pulse, Fft::dft_minus --
+ * the same radix-2 DIT as fft_plus with conjugated twiddles (proj/src/fft.cpp:30-51). */
+int oracle_range_fft(const double *cube_d, const ltci_radar *p, double *out) {
+    const int K = p->K;
+    if (K < 1 || (K & (K - 1))) return LTCI_INVALID_ARGUMENT;
+    size_t n = (size_t)K * p->M;
+    cplx *x = to_cplx(cube_d, n);
+    cplx *tw = twiddles(K);
+    for (int k = 0; k < K / 2; ++k) tw[k] = conj(tw[k]);
+    for (int m = 0; m < p->M; ++m) fft_plus(x + (size_t)m * K, K, tw);
+    for (size_t i = 0; i < n; ++i) {
+        out[2 * i] = creal(x[i]);
+        out[2 * i + 1] = cimag(x[i]);
+    }
+    free(tw);
+    free(x);
     return LTCI_OK;
 }

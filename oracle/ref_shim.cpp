@@ -318,6 +318,20 @@ int ref_keystone(const double* cube, const ltci_radar* r, int taps, double* out)
     return guarded([&] { copy_out(R::keystone(cube_of(cube, radar_of(*r)), taps).data, out); });
 }
 
+// range_fft / range_ifft (proj/src/signal_model.cpp:85-107)
+int ref_range_fft(const double* cube, const ltci_radar* r, double* out) {
+    return guarded([&] {
+        const R::RadarParams p = radar_of(*r);
+        R::RangePulseCube c(p);
+        std::memcpy(c.data.data(), cube, c.data.size() * sizeof(R::cplx));
+        copy_out(R::range_fft(c).data, out);
+    });
+}
+
+int ref_range_ifft(const double* cube, const ltci_radar* r, double* out) {
+    return guarded([&] { copy_out(R::range_ifft(cube_of(cube, radar_of(*r))).data, out); });
+}
+
 // mgift (proj/src/transforms.cpp:157-173)
 int ref_mgift(const double* cube, const ltci_radar* r, const double* ctilde, int n, int variant,
               double* out) {

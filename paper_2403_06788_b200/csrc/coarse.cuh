@@ -428,4 +428,119 @@ __global__ void __launch_bounds__(256) keystone_kernel(KeystoneArgs a) {
     }
 }
 
+// K4 tiled: the same resampling on 32-row x 64-pulse output tiles.  A CTA
+// stages the input pulses its tile can touch (the union over its rows of
+// [x_first - taps/2, x_last + taps/2], ~84 pulses at the BASELINE radars) as
+// 256-byte coalesced row segments in shared memory, all loads in flight at
+// once, then every lane (one frequency row) produces 8 outputs reading its
+// taps from shared memory (lane-contiguous, conflict-free) and storing
+// 256-byte coalesced rows.  Per output one FP64 multiply and round give j0
+// and frac; the weights avoid every per-tap transcendental and division:
+//   * sinc(frac + n) = (-1)^n sin(pi frac) / (pi (frac + n)); the factor
+//     sin(pi frac)/pi / prod_i (frac + i) is common to all taps and cancels in
+//     the unit-sum renormalisation, leaving (-1)^n prod_{i != n} (frac + i)
+//     (prefix x suffix products);
+//   * the Hamming window cos(pi (frac + n)/half) by angle addition from one
+//     sincospi(frac / half) and the per-CTA table cos/sin(pi n / half).
+// Tiles whose span exceeds the stage (very wide bands: fbar far from 1 across
+// the tile) read their taps straight from global memory instead.
+constexpr int kKtRows = 32, kKtTile = 64, kKtSpan = 96, kKtThreads = 256;
+
+template <int HALF, bool STAGED>
+__device__ __forceinline__ float2 keystone_point(const KeystoneArgs& a, const float2 (*s_in)[kKtRows],
+                                                 const float2* __restrict__ col, const float2 (&cb)[2 * HALF],
+                                                 double fbar, int m, int idx_lo, int lane) {
+    constexpr int NTAP = 2 * HALF;
+    const size_t K = static_cast<size_t>(a.K);
+    auto tap = [&](long long j1) -> float2 {  // sample at 0-based pulse clamp(j1)
+        const int src = static_cast<int>(min(max(j1, 0ll), static_cast<long long>(a.M - 1)));
+        return STAGED ? s_in[src - idx_lo][lane] : col[static_cast<size_t>(src) * K];
+    };
+    const double x = fbar * static_cast<double>(m + 1);
+    const long long j0 = llround(x);
+    if (x == static_cast<double>(j0)) return tap(j0 - 1);
+    const float fr = static_cast<float>(x - static_cast<double>(j0));
+    float sa, ca;
+    sincospif(fr / static_cast<float>(HALF), &sa, &ca);
+    // tap i: j = j0 - HALF + 1 + i, n = j0 - j = HALF - 1 - i, u = fr + n
+    float d[NTAP], pre[NTAP];
+    float acc_p = 1.0f;
+#pragma unroll
+    for (int i = 0; i < NTAP; ++i) {
+        d[i] = fr + static_cast<float>(HALF - 1 - i);
+        pre[i] = acc_p;
+        acc_p *= d[i];
+    }
+    float suf = 1.0f, wsum = 0.0f;
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = NTAP - 1; i >= 0; --i) {
+        const float win = fmaf(0.46f, fmaf(ca, cb[i].x, -sa * cb[i].y), 0.54f);
+        const float sgn = ((HALF - 1 - i) & 1) ? -1.0f : 1.0f;
+        const float w = sgn * win * (pre[i] * suf);
+        suf *= d[i];
+        wsum += w;
+        const float2 y = tap(j0 - HALF + i);  // 0-based index (j - 1)
+        acc.x = fmaf(w, y.x, acc.x);
+        acc.y = fmaf(w, y.y, acc.y);
+    }
+    const float inv = 1.0f / wsum;
+    return make_float2(acc.x * inv, acc.y * inv);
+}
+
+// grid: (ceil(K / 32), ceil(M / 64)), kKtThreads threads
+template <int HALF>
+__global__ void __launch_bounds__(kKtThreads) keystone_tiled_kernel(KeystoneArgs a) {
+    constexpr int NTAP = 2 * HALF;
+    __shared__ float2 s_in[kKtSpan][kKtRows];
+    __shared__ float2 s_cs[NTAP];  // (cos, sin)(pi n / HALF), n = HALF - 1 - i
+    __shared__ int s_lo, s_n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = blockIdx.x * kKtRows + lane;
+    const bool live = k < a.K;
+    const int m_a = blockIdx.y * kKtTile, m_b = min(a.M, m_a + kKtTile);
+    const double fk = a.delta_f * static_cast<double>(k < a.K / 2 ? k : k - a.K);
+    const double fbar = a.fc / (fk + a.fc);
+    if (threadIdx.x < NTAP) {
+        float sn, cs;
+        sincospif(static_cast<float>(HALF - 1 - static_cast<int>(threadIdx.x)) / static_cast<float>(HALF), &sn, &cs);
+        s_cs[threadIdx.x] = make_float2(cs, sn);
+    }
+    if (warp == 0) {
+        // the tile's input pulses: union over its rows of the tap windows, clamped
+        int lo = 0x7fffffff, hi = -0x7fffffff;
+        if (live) {
+            lo = static_cast<int>(llround(fbar * static_cast<double>(m_a + 1))) - HALF;
+            hi = static_cast<int>(llround(fbar * static_cast<double>(m_b))) + HALF - 1;
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (lane == 0) {
+            lo = min(max(lo, 0), a.M - 1);
+            hi = min(max(hi, 0), a.M - 1);
+            s_lo = lo;
+            s_n = hi - lo + 1;
+        }
+    }
+    __syncthreads();
+    const int idx_lo = s_lo, n = s_n;
+    const float2* __restrict__ col = a.in + (live ? k : 0);
+    const size_t K = static_cast<size_t>(a.K);
+    float2 cb[NTAP];
+#pragma unroll
+    for (int i = 0; i < NTAP; ++i) cb[i] = s_cs[i];
+    if (n <= kKtSpan) {
+        for (int i = warp; i < n; i += kKtThreads / 32)
+            s_in[i][lane] = live ? col[static_cast<size_t>(idx_lo + i) * K] : make_float2(0.f, 0.f);
+        __syncthreads();
+        if (!live) return;
+        for (int m = m_a + warp; m < m_b; m += kKtThreads / 32)
+            a.out[k + K * static_cast<size_t>(m)] = keystone_point<HALF, true>(a, s_in, col, cb, fbar, m, idx_lo, lane);
+    } else {
+        if (!live) return;
+        for (int m = m_a + warp; m < m_b; m += kKtThreads / 32)
+            a.out[k + K * static_cast<size_t>(m)] = keystone_point<HALF, false>(a, s_in, col, cb, fbar, m, 0, lane);
+    }
+}
+
 }  // namespace ltcib

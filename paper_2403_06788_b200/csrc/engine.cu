@@ -28,10 +28,12 @@
 
 #include "../../include/ltci_cuda.h"
 #include "coarse.cuh"
+#include "coarse2k.cuh"
 #include "cube_io.hpp"
 #include "fine_fft.cuh"
 #include "fine_tc.cuh"
 #include "fd_grft.cuh"
+#include "range_fft.cuh"
 
 using namespace ltcib;
 
@@ -370,6 +372,28 @@ void ensure_smem_attr(const void* kern, int bytes) {
 
 int coarse_pg(int K, int M) { return coarse_pg_for(K, M); }
 
+// K4 launch: the tiled kernel for 2..16 taps (HALF = taps / 2 <= 8), the
+// per-element kernel beyond
+void launch_keystone(const KeystoneArgs& ka, cudaStream_t st) {
+    const int half = ka.taps / 2;
+    const dim3 grid((ka.K + kKtRows - 1) / kKtRows, (ka.M + kKtTile - 1) / kKtTile);
+    switch (half) {
+        case 1: keystone_tiled_kernel<1><<<grid, kKtThreads, 0, st>>>(ka); break;
+        case 2: keystone_tiled_kernel<2><<<grid, kKtThreads, 0, st>>>(ka); break;
+        case 3: keystone_tiled_kernel<3><<<grid, kKtThreads, 0, st>>>(ka); break;
+        case 4: keystone_tiled_kernel<4><<<grid, kKtThreads, 0, st>>>(ka); break;
+        case 5: keystone_tiled_kernel<5><<<grid, kKtThreads, 0, st>>>(ka); break;
+        case 6: keystone_tiled_kernel<6><<<grid, kKtThreads, 0, st>>>(ka); break;
+        case 7: keystone_tiled_kernel<7><<<grid, kKtThreads, 0, st>>>(ka); break;
+        case 8: keystone_tiled_kernel<8><<<grid, kKtThreads, 0, st>>>(ka); break;
+        default: {
+            const size_t total = static_cast<size_t>(ka.K) * ka.M;
+            keystone_kernel<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16)), 256, 0, st>>>(ka);
+        }
+    }
+    CK(cudaGetLastError());
+}
+
 __global__ void module_anchor_kernel() {}
 
 // The runtime loads kernels lazily, on their first launch, so module-loading
@@ -422,8 +446,29 @@ void launch_coarse_k(const CoarseArgs& a, cudaStream_t st) {
     CK(cudaGetLastError());
 }
 
+// K = 2048, complex64 output (C1, C3): the specialised K1 (coarse2k.cuh);
+// LTCI_COARSE_GENERIC=1 selects the generic kernel for A/B runs
+bool coarse2k_selected() {
+    static const bool generic = [] {
+        const char* env = std::getenv("LTCI_COARSE_GENERIC");
+        return env && std::atoi(env) != 0;
+    }();
+    return !generic;
+}
+
+void launch_coarse2k(const CoarseArgs& a, cudaStream_t st) {
+    ensure_smem_attr(reinterpret_cast<const void*>(coarse2k_kernel), static_cast<int>(coarse2k_smem_bytes()));
+    dim3 grid(a.M / k2kPG, a.c_count);
+    coarse2k_kernel<<<grid, k2kThreads, coarse2k_smem_bytes(), st>>>(a);
+    CK(cudaGetLastError());
+}
+
 template <int OUT16>
 void launch_coarse_out(const CoarseArgs& a, cudaStream_t st) {
+    if (!OUT16 && a.K == 2048 && a.M >= k2kPG && coarse2k_selected()) {
+        launch_coarse2k(a, st);
+        return;
+    }
     switch (a.K) {
         case 16: launch_coarse_k<16, OUT16>(a, st); break;
         case 32: launch_coarse_k<32, OUT16>(a, st); break;
@@ -444,6 +489,41 @@ void launch_coarse(const CoarseArgs& a, int /*pg*/, cudaStream_t st, bool out16 
         launch_coarse_out<1>(a, st);
     else
         launch_coarse_out<0>(a, st);
+}
+
+// K0 range FFT launch (range-pulse -> freq-pulse, ltci::range_fft)
+template <int K, int IN64>
+void launch_range_fft_k(const void* in, float2* out, int M, cudaStream_t st) {
+    auto kern = range_fft_kernel<K, IN64>;
+    const size_t smem = range_fft_smem_bytes(K, M);
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), 96 * 1024);
+    const int pg = range_fft_pg(K, M);
+    range_fft_kernel<K, IN64><<<(M + pg - 1) / pg, kRangeFftThreads, smem, st>>>(in, out, M);
+    CK(cudaGetLastError());
+}
+
+template <int IN64>
+void launch_range_fft_in(const void* in, float2* out, int K, int M, cudaStream_t st) {
+    switch (K) {
+        case 16: launch_range_fft_k<16, IN64>(in, out, M, st); break;
+        case 32: launch_range_fft_k<32, IN64>(in, out, M, st); break;
+        case 64: launch_range_fft_k<64, IN64>(in, out, M, st); break;
+        case 128: launch_range_fft_k<128, IN64>(in, out, M, st); break;
+        case 256: launch_range_fft_k<256, IN64>(in, out, M, st); break;
+        case 512: launch_range_fft_k<512, IN64>(in, out, M, st); break;
+        case 1024: launch_range_fft_k<1024, IN64>(in, out, M, st); break;
+        case 2048: launch_range_fft_k<2048, IN64>(in, out, M, st); break;
+        case 4096: launch_range_fft_k<4096, IN64>(in, out, M, st); break;
+        case 8192: launch_range_fft_k<8192, IN64>(in, out, M, st); break;
+        default: fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: range_fft needs K a power of two in [16, 8192]");
+    }
+}
+
+void launch_range_fft(const void* in, bool in64, float2* out, int K, int M, cudaStream_t st) {
+    if (in64)
+        launch_range_fft_in<1>(in, out, K, M, st);
+    else
+        launch_range_fft_in<0>(in, out, K, M, st);
 }
 
 // ---- tcgen05 fine path: TMA tensor maps over the fp16 X planes ----------
@@ -628,6 +708,37 @@ struct DevBuf {
     ~DevBuf() { release(); }
 };
 
+// grow-only pinned host buffer (mapped when asked: small results are written
+// there by the device)
+template <typename T>
+struct HostBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t count, unsigned flags = cudaHostAllocDefault) {
+        if (count <= n) return;
+        release();
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), flags));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~HostBuf() { release(); }
+};
+
+// Pinned staging for H2D of a caller's pageable host cube: one host memcpy
+// into the block, then an async DMA (no driver-side pageable path).  The event
+// guards reuse: a block is refilled only after its previous DMA completed.
+struct Stager {
+    HostBuf<double2> buf;
+    cudaEvent_t ev = nullptr;
+    ~Stager() {
+        if (ev) cudaEventDestroy(ev);
+    }
+};
+
 }  // namespace
 
 void ltcib_set_last_error(const char* msg) { g_err = msg ? msg : ""; }
@@ -668,6 +779,10 @@ struct ltci_engine {
     double* stage[2] = {nullptr, nullptr};
     size_t stage_doubles = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+    // small-result fast path (mapped) and pinned staging for dense maps
+    HostBuf<unsigned char> small;
+    HostBuf<float2> dense_h;
+    Stager stager;
 };
 
 namespace {
@@ -680,6 +795,60 @@ struct DeviceGuard {
     }
     ~DeviceGuard() { cudaSetDevice(prev); }
 };
+
+// Bounded per-device pool of reusable objects (one-shot engines, fd_grft
+// workspaces).  A call leases one (or makes one), returns it afterwards; at
+// most LTCI_POOL_IDLE (default 2) idle objects per device are kept, the rest
+// are destroyed on return, so N calling threads never pin N x the buffers.
+template <typename T>
+struct ObjectPool {
+    std::mutex mu;
+    std::vector<std::vector<std::unique_ptr<T>>> idle;  // [device]
+    size_t cap = [] {
+        const char* env = std::getenv("LTCI_POOL_IDLE");
+        return env ? static_cast<size_t>(std::strtoull(env, nullptr, 10)) : size_t{2};
+    }();
+    std::unique_ptr<T> take(int device) {
+        std::lock_guard<std::mutex> g(mu);
+        if (static_cast<int>(idle.size()) <= device) idle.resize(device + 1);
+        auto& v = idle[device];
+        if (v.empty()) return std::make_unique<T>();
+        std::unique_ptr<T> o = std::move(v.back());
+        v.pop_back();
+        return o;
+    }
+    void give(int device, std::unique_ptr<T> o) {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            auto& v = idle[device];
+            if (v.size() < cap) {
+                v.push_back(std::move(o));
+                return;
+            }
+        }
+        DeviceGuard dg(device);
+        o.reset();  // frees the device buffers outside the lock
+    }
+    size_t idle_count(int device) {
+        std::lock_guard<std::mutex> g(mu);
+        return device < static_cast<int>(idle.size()) ? idle[device].size() : 0;
+    }
+};
+
+template <typename T>
+struct PoolLease {
+    ObjectPool<T>& pool;
+    int device;
+    std::unique_ptr<T> obj;
+    PoolLease(ObjectPool<T>& p, int dev) : pool(p), device(dev), obj(p.take(dev)) {}
+    ~PoolLease() { pool.give(device, std::move(obj)); }
+    T& operator*() { return *obj; }
+};
+
+ObjectPool<ltci_engine>& engine_pool() {
+    static auto* p = new ObjectPool<ltci_engine>();  // leaked: no teardown after the CUDA runtime
+    return *p;
+}
 
 void engine_init(ltci_engine* e) {
     const Plan& pl = e->pl;
@@ -725,7 +894,9 @@ void engine_init(ltci_engine* e) {
         e->X.ensure(e->batch * per_coarse / sizeof(float2));
     }
     const unsigned long long H = pl.coarse_cells * pl.fine_cells * pl.R_slice * pl.D;
-    e->cand_cap = std::max<unsigned long long>(1, std::min<unsigned long long>(H, 1ull << 22));
+    unsigned long long cap0 = 1ull << 22;  // initial candidate buffer (grown by the overflow re-run)
+    if (const char* env = std::getenv("LTCI_CAND_CAP")) cap0 = std::strtoull(env, nullptr, 10);
+    e->cand_cap = std::max<unsigned long long>(1, std::min<unsigned long long>(H, cap0));
     e->cand.ensure(e->cand_cap);
     if (pl.keep_dense) {
         const unsigned long long cells = pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D;
@@ -775,10 +946,7 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
             kt_ev = {evi, evi + 1};
             CK(cudaEventRecord(e->ev[evi], st));
         }
-        const size_t total = static_cast<size_t>(K) * M;
-        const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16));
-        keystone_kernel<<<blocks, 256, 0, st>>>(ka);
-        CK(cudaGetLastError());
+        launch_keystone(ka, st);
         ++e->launches;
         if (kt_ev.first >= 0) {
             CK(cudaEventRecord(e->ev[evi + 1], st));
@@ -909,7 +1077,16 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
             fine_ev.push_back({evc + 2, evc + 3});
         }
     }
-    e->last_cube = d_cube;
+    if (d_cube != e->cube_c64.p) {
+        // The candidate-overflow re-run in assemble() must see this run's echo,
+        // not whatever a caller-owned buffer holds by the time result() is
+        // called (double-buffered CPI streams reuse it): keep a private copy,
+        // queued behind the run so it costs no latency (~5 us at C1).
+        const size_t n = static_cast<size_t>(K) * M;
+        e->cube_c64.ensure(n);
+        CK(cudaMemcpyAsync(e->cube_c64.p, d_cube, n * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+    }
+    e->last_cube = e->cube_c64.p;
     e->ran = true;
     if (tm) {
         CK(cudaStreamSynchronize(st));
@@ -930,11 +1107,32 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
     }
 }
 
+// H2D of a host float64 cube: pinned (or registered) memory goes straight to
+// the DMA engine; small pageable cubes (<= 8 MiB, the one-shot drop-in calls
+// of Monte-Carlo loops) are staged through a pinned block; large pageable
+// cubes go direct (the driver pipelines them).
+void h2d_cube(double2* dst, const double* src, size_t n, Stager& sg, cudaStream_t st) {
+    const size_t bytes = n * sizeof(double2);
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // unregistered pointers may leave an error behind on old runtimes
+    if (pinned || bytes > (8u << 20)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    if (!sg.ev) CK(cudaEventCreateWithFlags(&sg.ev, cudaEventDisableTiming));
+    CK(cudaEventSynchronize(sg.ev));  // the block's previous DMA is done
+    sg.buf.ensure(n);
+    std::memcpy(sg.buf.p, src, bytes);
+    CK(cudaMemcpyAsync(dst, sg.buf.p, bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(sg.ev, st));
+}
+
 void upload_host_cube(ltci_engine* e, const double* cube, cudaStream_t st) {
     const size_t n = static_cast<size_t>(e->pl.rp.K) * e->pl.rp.M;
     e->cube_f64.ensure(n);
     e->cube_c64.ensure(n);
-    CK(cudaMemcpyAsync(e->cube_f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice, st));
+    h2d_cube(e->cube_f64.p, cube, n, e->stager, st);
     const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8));
     f64_to_c64_kernel<<<blocks, 256, 0, st>>>(e->cube_f64.p, e->cube_c64.p, n);
     CK(cudaGetLastError());
@@ -1017,22 +1215,122 @@ void sort_candidates(const CandRec* d_cand, unsigned long long count, unsigned l
     CK(cudaStreamSynchronize(st));
 }
 
+// ---- small-result fast path --------------------------------------------------
+// One kernel turns a run's reduced output into host-visible results: the
+// retained-candidate count, the peak slots, and -- when at most kSmallCand
+// cells were retained (the normal case at a sensible threshold) -- the
+// candidates sorted by flat index (bitonic sort in shared memory) and
+// recentred in FP64 with the same expression as cand_recenter_kernel, so the
+// values are bit-identical whichever path produced them.  It writes straight
+// into mapped pinned host memory, so a detector call needs one
+// synchronisation instead of a D2H round trip per array plus the multi-kernel
+// radix sort (which stays the path for larger candidate sets).
+constexpr unsigned long long kSmallCand = 2048;  // 32 KB of static shared memory
+
+
+// mapped result block: [u64 count, pad x7][n_slots PeakSlot][kSmallCand u64 idx][kSmallCand double2 val]
+struct SmallLayout {
+    size_t slots, idx, val, bytes;
+    explicit SmallLayout(int n_slots) {
+        slots = 64;
+        idx = slots + static_cast<size_t>(n_slots) * sizeof(PeakSlot);
+        val = idx + kSmallCand * sizeof(unsigned long long);
+        bytes = val + kSmallCand * sizeof(double2);
+    }
+};
+
+__global__ void __launch_bounds__(1024) small_result_kernel(const unsigned long long* __restrict__ count_p,
+                                                            const CandRec* __restrict__ cand,
+                                                            unsigned long long limit, const PeakSlot* __restrict__ slots,
+                                                            int n_slots, int D, int dop_first, int M,
+                                                            unsigned char* __restrict__ out, SmallLayout L) {
+    __shared__ unsigned long long key[kSmallCand];
+    __shared__ float2 val[kSmallCand];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const unsigned long long count = *count_p;
+    auto* h_slots = reinterpret_cast<PeakSlot*>(out + L.slots);
+    for (int r = tid; r < n_slots; r += nt) h_slots[r] = slots[r];
+    if (tid == 0) reinterpret_cast<unsigned long long*>(out)[0] = count;
+    if (count > limit || count == 0) return;  // host falls back (or nothing to sort)
+    const int n = static_cast<int>(count);
+    int N = 2;
+    while (N < n) N <<= 1;
+    for (int i = tid; i < N; i += nt) {
+        if (i < n) {
+            const CandRec c = cand[i];
+            key[i] = c.idx;
+            val[i] = make_float2(c.re, c.im);
+        } else {
+            key[i] = ~0ull;  // flat indices are < 2^64 - 1 and unique
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= N; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < N; i += nt) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const unsigned long long a = key[i], b = key[ixj];
+                    if ((a > b) == up) {
+                        key[i] = b;
+                        key[ixj] = a;
+                        const float2 t = val[i];
+                        val[i] = val[ixj];
+                        val[ixj] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    auto* h_idx = reinterpret_cast<unsigned long long*>(out + L.idx);
+    auto* h_val = reinterpret_cast<double2*>(out + L.val);
+    for (int i = tid; i < n; i += nt) {
+        const unsigned long long kk = key[i];
+        const int jj = static_cast<int>(kk % static_cast<unsigned long long>(D));
+        const int d = dop_first + jj - M / 2;
+        double sn, cs;
+        sincospi(2.0 * d / M, &sn, &cs);
+        const double re = val[i].x, im = val[i].y;
+        h_idx[i] = kk;
+        h_val[i] = make_double2(re * cs - im * sn, re * sn + im * cs);
+    }
+}
+
+// Enqueue the fast path into a (grow-only) mapped block; returns its host pointer.
+unsigned char* enqueue_small_result(HostBuf<unsigned char>& buf, const unsigned long long* d_count,
+                                    const CandRec* d_cand, unsigned long long cand_cap, const PeakSlot* d_slots,
+                                    int n_slots, int D, int dop_first, int M, cudaStream_t st) {
+    const SmallLayout L(n_slots);
+    buf.ensure(L.bytes, cudaHostAllocMapped);
+    unsigned char* dptr = nullptr;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), buf.p, 0));
+    small_result_kernel<<<1, 1024, 0, st>>>(d_count, d_cand, std::min(kSmallCand, cand_cap), d_slots, n_slots, D,
+                                           dop_first, M, dptr, L);
+    CK(cudaGetLastError());
+    return buf.p;
+}
+
 ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
     const Plan& pl = e->pl;
     DeviceGuard dg(e->device);
+    // the count, the per-row peak slots, small candidate sets (sorted and
+    // recentred) and the optional dense map come back behind one
+    // synchronisation (re-fetched below in the rare re-run case)
+    const SmallLayout L(pl.R_slice);
+    const size_t nd = pl.keep_dense ? static_cast<size_t>(pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D) : 0;
+    unsigned char* hb = nullptr;
     unsigned long long count = 0;
-    // the count, the per-row peak slots and the optional dense map come back
-    // behind one synchronisation (re-copied below in the rare re-run case)
-    std::vector<PeakSlot> slots(pl.R_slice);
-    std::vector<float2> dense;
     auto fetch = [&] {
-        CK(cudaMemcpyAsync(&count, e->cand_count.p, sizeof(count), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(slots.data(), e->slots.p, slots.size() * sizeof(PeakSlot), cudaMemcpyDeviceToHost, st));
-        if (pl.keep_dense) {
-            dense.resize(static_cast<size_t>(pl.coarse_cells * pl.fine_cells * pl.R_total * pl.D));  // not the (grow-only) buffer
-            CK(cudaMemcpyAsync(dense.data(), e->dense.p, dense.size() * sizeof(float2), cudaMemcpyDeviceToHost, st));
+        hb = enqueue_small_result(e->small, e->cand_count.p, e->cand.p, e->cand_cap, e->slots.p, pl.R_slice, pl.D,
+                                  pl.dop_first, pl.rp.M, st);
+        if (nd) {
+            e->dense_h.ensure(nd);  // not the (grow-only) device buffer's size
+            CK(cudaMemcpyAsync(e->dense_h.p, e->dense.p, nd * sizeof(float2), cudaMemcpyDeviceToHost, st));
         }
         CK(cudaStreamSynchronize(st));
+        count = *reinterpret_cast<volatile unsigned long long*>(hb);
     };
     fetch();
     if (count > e->cand_cap) {
@@ -1051,6 +1349,7 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         run_device_impl(e, e->last_cube, st);
         fetch();
     }
+    const PeakSlot* slots = reinterpret_cast<const PeakSlot*>(hb + L.slots);
 
     auto* out = static_cast<ltci_detection_map*>(std::calloc(1, sizeof(ltci_detection_map)));
     if (!out) throw std::bad_alloc();
@@ -1088,7 +1387,10 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         out->n_candidates = count;
         out->cand_index = static_cast<uint64_t*>(xmalloc(count * sizeof(uint64_t)));
         out->cand_value = static_cast<double*>(xmalloc(2 * count * sizeof(double)));
-        if (count) {
+        if (count && count <= std::min(kSmallCand, e->cand_cap)) {
+            std::memcpy(out->cand_index, hb + L.idx, count * sizeof(uint64_t));
+            std::memcpy(out->cand_value, hb + L.val, count * sizeof(double2));
+        } else if (count) {
             const unsigned long long cells = static_cast<unsigned long long>(pl.coarse_cells) * pl.fine_cells *
                                              static_cast<unsigned long long>(pl.R_total) * pl.D;
             CandSortBufs b{e->ck0, e->ck1, e->cv0, e->cv1, e->cvals, e->csort_tmp};
@@ -1097,9 +1399,10 @@ ltci_detection_map* assemble(ltci_engine* e, cudaStream_t st) {
         }
         if (pl.keep_dense) {
             out->dense_stored = 1;
-            out->dense_count = dense.size();
-            out->dense = static_cast<double*>(xmalloc(2 * dense.size() * sizeof(double)));
-            for (size_t i = 0; i < dense.size(); ++i) recenter(pl, i, dense[i].x, dense[i].y, out->dense + 2 * i);
+            out->dense_count = nd;
+            out->dense = static_cast<double*>(xmalloc(2 * nd * sizeof(double)));
+            const float2* dh = e->dense_h.p;
+            for (size_t i = 0; i < nd; ++i) recenter(pl, i, dh[i].x, dh[i].y, out->dense + 2 * i);
         }
     } catch (...) {
         ltci_cuda_free_map(out);
@@ -1114,13 +1417,14 @@ int detect(const double* cube, const ltci_radar* cp, const ltci_ambiguity* amb, 
         if (!cube || !cp || !s || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
         const int device = opt ? opt->device : 0;
         if (device < 0) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad device ordinal");
-        // One-shot calls reuse a per-thread, per-device engine: its device
-        // buffers only grow, so a stream of small calls (Monte-Carlo trials,
-        // the reference's timing loops) pays no cudaMalloc/cudaFree per call.
-        thread_local std::vector<std::unique_ptr<ltci_engine>> pool;
-        if (static_cast<int>(pool.size()) <= device) pool.resize(device + 1);
-        if (!pool[device]) pool[device] = std::make_unique<ltci_engine>();
-        ltci_engine& eng = *pool[device];
+        // One-shot calls lease an engine from a process-wide, per-device pool:
+        // its device buffers only grow, so a stream of small calls
+        // (Monte-Carlo trials, the reference's timing loops) pays no
+        // cudaMalloc/cudaFree per call, while the number of idle engines kept
+        // is bounded (LTCI_POOL_IDLE, default 2 per device) however many host
+        // threads fan calls out (proj/src/bench.cpp:94-110).
+        PoolLease<ltci_engine> lease(engine_pool(), device);
+        ltci_engine& eng = *lease;
         static const bool trace = std::getenv("LTCI_TRACE") != nullptr;  // per-phase wall times on stderr
         using clk = std::chrono::steady_clock;
         const auto t0 = clk::now();
@@ -1214,6 +1518,25 @@ void fd_launch(const FdArgs& a, cudaStream_t st) {
     }
 }
 
+struct FdWorkspace {
+    DevBuf<double2> f64;
+    DevBuf<float2> c64, acc, dense;
+    DevBuf<CandRec> cand;
+    DevBuf<unsigned long long> ccount, k0, k1;
+    DevBuf<PeakSlot> best;
+    DevBuf<float2> v0, v1;
+    DevBuf<double2> vo;
+    DevBuf<unsigned char> tmp;
+    HostBuf<unsigned char> small;
+    HostBuf<float2> dense_h;
+    Stager stager;
+};
+
+ObjectPool<FdWorkspace>& fd_pool() {
+    static auto* p = new ObjectPool<FdWorkspace>();  // leaked: no teardown after the CUDA runtime
+    return *p;
+}
+
 ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const ltci_radar& rp,
                                 const ltci_single_space& s, const ltci_options* opt) {
     validate_radar(rp);
@@ -1242,22 +1565,11 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
     cudaStream_t st = nullptr;
     const int K = rp.K, M = rp.M;
     const size_t n = static_cast<size_t>(K) * M;
-    // per-thread, per-device workspace: grow-only buffers reused across calls
-    // (many small calls -- e.g. noise-only Monte-Carlo trials -- pay no cudaMalloc)
-    struct FdWorkspace {
-        DevBuf<double2> f64;
-        DevBuf<float2> c64, acc, dense;
-        DevBuf<CandRec> cand;
-        DevBuf<unsigned long long> ccount, k0, k1;
-        DevBuf<PeakSlot> best;
-        DevBuf<float2> v0, v1;
-        DevBuf<double2> vo;
-        DevBuf<unsigned char> tmp;
-    };
-    thread_local std::vector<std::unique_ptr<FdWorkspace>> pool;
-    if (static_cast<int>(pool.size()) <= device) pool.resize(device + 1);
-    if (!pool[device]) pool[device] = std::make_unique<FdWorkspace>();
-    FdWorkspace& w = *pool[device];
+    // per-device workspace leased from a bounded process-wide pool: grow-only
+    // buffers reused across calls (many small calls -- e.g. noise-only
+    // Monte-Carlo trials -- pay no cudaMalloc), at most LTCI_POOL_IDLE idle
+    PoolLease<FdWorkspace> lease(fd_pool(), device);
+    FdWorkspace& w = *lease;
     auto& f64 = w.f64;
     auto& c64 = w.c64;
     auto& acc = w.acc;
@@ -1268,18 +1580,21 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
     if (!d_cube) {
         f64.ensure(n);
         c64.ensure(n);
-        CK(cudaMemcpyAsync(f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice, st));
+        h2d_cube(f64.p, cube, n, w.stager, st);
         f64_to_c64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(f64.p, c64.p,
                                                                                                           n);
         CK(cudaGetLastError());
     }
 
     size_t free_b = 0, total_b = 0;
+    const size_t nd = keep_dense ? static_cast<size_t>(cells) * R : 0;
     if (keep_dense) {
-        CK(cudaMemGetInfo(&free_b, &total_b));
-        const double bytes = static_cast<double>(cells) * R * sizeof(float2);
-        if (bytes > 0.5 * static_cast<double>(free_b) || bytes * 2 > 64.0 * (1ull << 30))
-            fail(LTCI_BAD_ALLOC, "ltci_cuda: dense fd_grft map exceeds the result memory");
+        const double bytes = static_cast<double>(nd) * sizeof(float2);
+        if (bytes > static_cast<double>(256u << 20)) {  // the (slow) memory query only for big maps
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            if (bytes > 0.5 * static_cast<double>(free_b) || bytes * 2 > 64.0 * (1ull << 30))
+                fail(LTCI_BAD_ALLOC, "ltci_cuda: dense fd_grft map exceeds the result memory");
+        }
         dense.ensure(static_cast<size_t>(cells) * R);
     }
     // MF output per batch: bounded at 2 GiB, whole CTAs of both kernels
@@ -1312,20 +1627,28 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
     a.cand_count = ccount.p;
 
     unsigned long long cap = std::max<unsigned long long>(cand.n, 1ull << 16), count = 0;
+    const SmallLayout L(1);
+    unsigned char* hb = nullptr;
     for (int attempt = 0; attempt < 2; ++attempt) {
         cand.ensure(cap);
         a.cand = cand.p;
         a.cand_cap = cap;
         CK(cudaMemsetAsync(ccount.p, 0, sizeof(unsigned long long), st));
-        const PeakSlot init{0.f, 0.f, ~0ull};
-        CK(cudaMemcpyAsync(best.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+        init_slots_kernel<<<1, 32, 0, st>>>(best.p, 1);
+        CK(cudaGetLastError());
         for (unsigned long long c0 = 0; c0 < cells; c0 += batch) {
             a.c_begin = c0;
             a.c_count = std::min(batch, cells - c0);
             fd_launch(a, st);
         }
-        CK(cudaMemcpyAsync(&count, ccount.p, sizeof(count), cudaMemcpyDeviceToHost, st));
+        // count, best cell and small candidate sets behind one synchronisation
+        hb = enqueue_small_result(w.small, ccount.p, cand.p, cap, best.p, 1, 1, M / 2, M, st);
+        if (nd) {
+            w.dense_h.ensure(nd);
+            CK(cudaMemcpyAsync(w.dense_h.p, dense.p, nd * sizeof(float2), cudaMemcpyDeviceToHost, st));
+        }
         CK(cudaStreamSynchronize(st));
+        count = *reinterpret_cast<volatile unsigned long long*>(hb);
         if (count <= cap) break;
         CK(cudaMemGetInfo(&free_b, &total_b));
         if (static_cast<double>(count) * 64.0 > 0.8 * static_cast<double>(free_b) ||
@@ -1348,23 +1671,23 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
         out->counters[1] = cells * static_cast<unsigned long long>(K);  // mf += n0() per cell
         out->counters[2] = cells;                                       // ifft += 1 per cell
         out->retain_threshold = retain;
-        PeakSlot b{};
-        CK(cudaMemcpy(&b, best.p, sizeof(b), cudaMemcpyDeviceToHost));
+        const PeakSlot b = *reinterpret_cast<const PeakSlot*>(hb + L.slots);
         out->argmax = b.idx;
         out->argmax_value[0] = b.re;
         out->argmax_value[1] = b.im;
         out->n_candidates = count;
         out->cand_index = static_cast<uint64_t*>(xmalloc(count * sizeof(uint64_t)));
         out->cand_value = static_cast<double*>(xmalloc(2 * count * sizeof(double)));
-        if (count) {
+        if (count && count <= std::min(kSmallCand, cap)) {
+            std::memcpy(out->cand_index, hb + L.idx, count * sizeof(uint64_t));
+            std::memcpy(out->cand_value, hb + L.val, count * sizeof(double2));
+        } else if (count) {
             CandSortBufs bufs{w.k0, w.k1, w.v0, w.v1, w.vo, w.tmp};
             sort_candidates(cand.p, count, cells * static_cast<unsigned long long>(R), 1, M / 2, M, bufs,
                             out->cand_index, out->cand_value, st);
         }
         if (keep_dense) {
-            const size_t nd = static_cast<size_t>(cells) * R;
-            std::vector<float2> h(nd);
-            CK(cudaMemcpy(h.data(), dense.p, nd * sizeof(float2), cudaMemcpyDeviceToHost));
+            const float2* h = w.dense_h.p;
             out->dense_stored = 1;
             out->dense_count = nd;
             out->dense = static_cast<double*>(xmalloc(2 * nd * sizeof(double)));
@@ -1501,14 +1824,54 @@ int ltci_cuda_keystone(const double* cube, const ltci_radar* p, int taps, double
         CK(cudaMemcpy(f64.p, cube, n * sizeof(double2), cudaMemcpyHostToDevice));
         f64_to_c64_kernel<<<256, 256>>>(f64.p, a.p, n);
         KeystoneArgs ka{a.p, b.p, p->K, p->M, taps, p->fc, p->delta_f};
-        keystone_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)), 256>>>(ka);
-        CK(cudaGetLastError());
+        launch_keystone(ka, nullptr);
         std::vector<float2> h(n);
         CK(cudaMemcpy(h.data(), b.p, n * sizeof(float2), cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < n; ++i) {
             out[2 * i] = h[i].x;
             out[2 * i + 1] = h[i].y;
         }
+    });
+}
+
+int ltci_cuda_range_fft(const double* range_cube, const ltci_radar* p, double* out) {
+    return guarded([&] {
+        if (!range_cube || !p || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        validate_radar(*p);
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(LTCI_NO_DEVICE, "ltci_cuda: no CUDA device available");
+        const size_t n = static_cast<size_t>(p->K) * p->M;
+        DevBuf<double2> f64;
+        DevBuf<float2> b;
+        f64.ensure(n);
+        b.ensure(n);
+        CK(cudaMemcpy(f64.p, range_cube, n * sizeof(double2), cudaMemcpyHostToDevice));
+        launch_range_fft(f64.p, true, b.p, p->K, p->M, nullptr);
+        std::vector<float2> h(n);
+        CK(cudaMemcpy(h.data(), b.p, n * sizeof(float2), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i) {
+            out[2 * i] = h[i].x;
+            out[2 * i + 1] = h[i].y;
+        }
+    });
+}
+
+int ltci_cuda_range_fft_device(const void* d_in, void* d_out, const ltci_radar* p, void* stream) {
+    return guarded([&] {
+        if (!d_in || !d_out || !p) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        validate_radar(*p);
+        launch_range_fft(d_in, false, static_cast<float2*>(d_out), p->K, p->M, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ltci_cuda_keystone_device(const void* d_in, void* d_out, const ltci_radar* p, int taps, void* stream) {
+    return guarded([&] {
+        if (!d_in || !d_out || !p) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        validate_radar(*p);
+        if (taps < 2) fail(LTCI_INVALID_ARGUMENT, "keystone: need at least 2 taps");
+        KeystoneArgs ka{static_cast<const float2*>(d_in), static_cast<float2*>(d_out), p->K, p->M, taps, p->fc,
+                        p->delta_f};
+        launch_keystone(ka, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1653,6 +2016,14 @@ int ltci_cuda_gft(const double* rows, const ltci_radar* p, const double* fine_hi
     });
 }
 
+int ltci_cuda_pool_idle(int device, int64_t* engines, int64_t* fd_workspaces) {
+    return guarded([&] {
+        if (device < 0) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: bad device ordinal");
+        if (engines) *engines = static_cast<int64_t>(engine_pool().idle_count(device));
+        if (fd_workspaces) *fd_workspaces = static_cast<int64_t>(fd_pool().idle_count(device));
+    });
+}
+
 int ltci_engine_create(const ltci_radar* p, const ltci_dual_space* space, const ltci_ambiguity* amb, int variant,
                        const ltci_options* opt, int row_begin, int row_end, ltci_engine** out) {
     return guarded([&] {
@@ -1702,6 +2073,38 @@ int ltci_engine_run_host(ltci_engine* e, const double* cube, void* stream) {
     });
 }
 
+// configs[3] front end: a range-pulse (fast-time) cube goes through K0
+// (range_fft, reference proj/src/signal_model.cpp:97-107) into the engine's
+// own freq-pulse buffer, then the cascade runs on it.
+int ltci_engine_run_range_device(ltci_engine* e, const void* d_range_c64, void* stream) {
+    return guarded([&] {
+        if (!e || !d_range_c64) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        DeviceGuard dg(e->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t n = static_cast<size_t>(e->pl.rp.K) * e->pl.rp.M;
+        e->cube_c64.ensure(n);
+        launch_range_fft(d_range_c64, false, e->cube_c64.p, e->pl.rp.K, e->pl.rp.M, st);
+        run_device_impl(e, e->cube_c64.p, st);
+        e->launches += 1;  // K0
+    });
+}
+
+int ltci_engine_run_range_host(ltci_engine* e, const double* range_cube, void* stream) {
+    return guarded([&] {
+        if (!e || !range_cube) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        DeviceGuard dg(e->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t n = static_cast<size_t>(e->pl.rp.K) * e->pl.rp.M;
+        e->cube_f64.ensure(n);
+        e->cube_c64.ensure(n);
+        h2d_cube(e->cube_f64.p, range_cube, n, e->stager, st);
+        // the f64 -> c64 conversion is folded into K0's loads
+        launch_range_fft(e->cube_f64.p, true, e->cube_c64.p, e->pl.rp.K, e->pl.rp.M, st);
+        run_device_impl(e, e->cube_c64.p, st);
+        e->launches += 1;  // K0
+    });
+}
+
 // The wire path: file -> two pinned staging blocks ->
 // async H2D into the f64 echo buffer, the fread of block i+1 overlapping the
 // DMA of block i; then f64 -> c64 on the device and the detector run.
@@ -1731,7 +2134,9 @@ int ltci_engine_run_file(ltci_engine* e, const char* path, void* stream) {
         int b = 0;
         for (size_t off = 0, i = 0; off < total; off += e->stage_doubles, ++i, b ^= 1) {
             const size_t m = std::min(e->stage_doubles, total - off);
-            if (i >= 2) CK(cudaEventSynchronize(e->stage_ev[b]));  // block b's previous DMA done
+            // block b's previous DMA -- possibly queued by an earlier run_file call
+            // behind that call's kernels -- must be done before it is refilled
+            CK(cudaEventSynchronize(e->stage_ev[b]));
             rd.read(e->stage[b], m);
             CK(cudaMemcpyAsync(dst + off, e->stage[b], m * sizeof(double), cudaMemcpyHostToDevice, st));
             CK(cudaEventRecord(e->stage_ev[b], st));

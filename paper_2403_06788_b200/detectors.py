@@ -97,6 +97,18 @@ def keystone(cube: np.ndarray, params: RadarParams, taps: int = 8) -> np.ndarray
     return out
 
 
+def range_fft(range_cube: np.ndarray, params: RadarParams) -> np.ndarray:
+    """ltci::range_fft (proj/src/signal_model.cpp:97-107): per pulse the
+    unnormalised forward K-point DFT of a range-pulse cube (M, K) -> the
+    freq-pulse cube the detectors take (K0 on the device, complex64-exact)."""
+    lib = _lib.load()
+    data = np.ascontiguousarray(range_cube, dtype=np.complex128)
+    out = np.zeros_like(data)
+    r = params.to_c()
+    _lib.raise_for(lib.ltci_cuda_range_fft(_f64_ptr(data), C.byref(r), _f64_ptr(out)), lib)
+    return out
+
+
 def mgift(cube: np.ndarray, params: RadarParams, ctilde: Sequence[float], variant: int = A.VARIANT_GRFT) -> np.ndarray:
     """Returns the RangePulseCube as complex (M, K): [m, n]."""
     lib = _lib.load()
@@ -164,6 +176,21 @@ class Engine:
     def run_host(self, cube: np.ndarray, stream: int = 0):
         data = cube if (cube.dtype == np.complex128 and cube.flags.c_contiguous) else cube_as_f64(cube, self.params)
         _lib.raise_for(self._lib.ltci_engine_run_host(self._h, _f64_ptr(data), C.c_void_p(stream)), self._lib)
+
+    def run_range_device(self, d_range_ptr: int, stream: int = 0):
+        """configs[3] front end: K0 range FFT of a device complex64 RANGE-pulse cube, then the cascade."""
+        _lib.raise_for(self._lib.ltci_engine_run_range_device(self._h, C.c_void_p(d_range_ptr), C.c_void_p(stream)),
+                       self._lib)
+
+    def run_range_host(self, range_cube: np.ndarray, stream: int = 0):
+        """K0 + cascade from a host RANGE-pulse cube (M, K) complex."""
+        data = np.ascontiguousarray(range_cube, dtype=np.complex128)
+        _lib.raise_for(self._lib.ltci_engine_run_range_host(self._h, _f64_ptr(data), C.c_void_p(stream)), self._lib)
+
+    def run_range_host_ptr(self, host_ptr: int, stream: int = 0):
+        """K0 + cascade from a (pinned) host float64 interleaved RANGE-pulse buffer given by address."""
+        _lib.raise_for(self._lib.ltci_engine_run_range_host(self._h, C.c_void_p(host_ptr), C.c_void_p(stream)),
+                       self._lib)
 
     def run_host_ptr(self, host_ptr: int, stream: int = 0):
         """Run from a (pinned) host float64 interleaved buffer given by address."""

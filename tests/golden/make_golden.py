@@ -20,8 +20,11 @@ what the reference's own functions return:
   fd.npz           fd_grft at orders 1, 2 and 3 on
                    build_single_scale spaces, keep_dense + candidates; the order-2
                    case with a sub-ROI
+  range_fft.npz    range_fft (the configs[3] front end K0) of seeded range-pulse
+                   cubes: a noise cube, and range_ifft of a synthesized
+                   DS-KT-MFP scene (K_valid < K guard band) with its round trip
 
-    python tests/golden/make_golden.py [fd]     (fd: only fd.npz)
+    python tests/golden/make_golden.py [fd|range]     (fd / range: only that file)
 """
 from __future__ import annotations
 
@@ -89,11 +92,28 @@ def make_fd():
     np.savez_compressed(os.path.join(HERE, "fd.npz"), **out)
 
 
+def make_range():
+    # noise cube straight in the range domain, and a C3-like scene (fs > Br) taken
+    # to the range domain by the reference's range_ifft
+    p = O.ref_radar(3e9, 25e6, 20e6, 1000.0, 16, 128)
+    noise = c64(scene.add_noise(np.zeros((p.M, p.K), complex), 1.0, 303))
+    tgt = [(0.5 + 0.2j, [40 * p.delta_R(), 31.0, 2.5]), (0.3 - 0.1j, [90.4 * p.delta_R(), -55.0, -4.0])]
+    freq = c64(O.ref_synthesize(p, tgt, 1.0 / p.K, 404))
+    rng_scene = c64(O.ref_range_ifft(freq, p))
+    np.savez_compressed(os.path.join(HERE, "range_fft.npz"), noise=noise.astype(np.complex64),
+                        noise_fft=O.ref_range_fft(noise, p), scene_range=rng_scene.astype(np.complex64),
+                        scene_fft=O.ref_range_fft(rng_scene, p), **radar_arrays("", p))
+
+
 def main():
     assert O.have_ref(), "build the reference first: make -C oracle"
     if sys.argv[1:] == ["fd"]:
         make_fd()
         print("fd.npz written to", HERE)
+        return
+    if sys.argv[1:] == ["range"]:
+        make_range()
+        print("range_fft.npz written to", HERE)
         return
     # ---- transforms
     p = O.ref_radar(4 * 100e6, 100e6, 50e6, 2000.0, 32, 64)
@@ -146,6 +166,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "c0.npz"), cube=cube.astype(np.complex64), gamma=np.array(gamma),
                         peak_index=pi, peak_value=pv, **map_arrays("", m))
     make_fd()
+    make_range()
     print("golden vectors written to", HERE)
 
 
