@@ -446,23 +446,32 @@ __global__ void __launch_bounds__(256) keystone_kernel(KeystoneArgs a) {
 // the tile) read their taps straight from global memory instead.
 constexpr int kKtRows = 32, kKtTile = 64, kKtSpan = 96, kKtThreads = 256;
 
-template <int HALF, bool STAGED>
+// one output at pulse m, j0 = lround(fbar (m + 1)) and frac given: the taps
+// from shared memory (STAGED) or global memory, clamped to [0, M) when CLAMP.
+// cw[i] = (-1)^n (0.54, 0.46 cos, -0.46 sin)(pi n / half) folds the tap sign
+// into the Hamming window, evaluated by angle addition from one MUFU sin/cos
+// of pi frac / half.
+template <int HALF, bool STAGED, bool CLAMP>
 __device__ __forceinline__ float2 keystone_point(const KeystoneArgs& a, const float2 (*s_in)[kKtRows],
-                                                 const float2* __restrict__ col, const float2 (&cb)[2 * HALF],
-                                                 double fbar, int m, int idx_lo, int lane) {
+                                                 const float2* __restrict__ col, const float3 (&cw)[2 * HALF],
+                                                 int j0, float fr, int idx_lo, int lane) {
     constexpr int NTAP = 2 * HALF;
     const size_t K = static_cast<size_t>(a.K);
-    auto tap = [&](long long j1) -> float2 {  // sample at 0-based pulse clamp(j1)
-        const int src = static_cast<int>(min(max(j1, 0ll), static_cast<long long>(a.M - 1)));
-        return STAGED ? s_in[src - idx_lo][lane] : col[static_cast<size_t>(src) * K];
+    // tap i reads 0-based pulse j0 - HALF + i (= j - 1, j = j0 - HALF + 1 + i)
+    const float2* sp = STAGED && !CLAMP ? &s_in[j0 - HALF - idx_lo][lane] : nullptr;
+    auto tap = [&](int i) -> float2 {
+        if constexpr (STAGED && !CLAMP) {
+            return sp[i * kKtRows];
+        } else {
+            const int j1 = j0 - HALF + i;
+            const int src = CLAMP ? min(max(j1, 0), a.M - 1) : j1;
+            return STAGED ? s_in[src - idx_lo][lane] : col[static_cast<size_t>(src) * K];
+        }
     };
-    const double x = fbar * static_cast<double>(m + 1);
-    const long long j0 = llround(x);
-    if (x == static_cast<double>(j0)) return tap(j0 - 1);
-    const float fr = static_cast<float>(x - static_cast<double>(j0));
+    if (fr == 0.0f) return tap(HALF - 1);  // exact copy of pulse j0 - 1
     float sa, ca;
-    sincospif(fr / static_cast<float>(HALF), &sa, &ca);
-    // tap i: j = j0 - HALF + 1 + i, n = j0 - j = HALF - 1 - i, u = fr + n
+    __sincosf(fr * (3.14159265358979323846f / static_cast<float>(HALF)), &sa, &ca);
+    // tap i: n = j0 - j = HALF - 1 - i, u = fr + n
     float d[NTAP], pre[NTAP];
     float acc_p = 1.0f;
 #pragma unroll
@@ -475,47 +484,54 @@ __device__ __forceinline__ float2 keystone_point(const KeystoneArgs& a, const fl
     float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = NTAP - 1; i >= 0; --i) {
-        const float win = fmaf(0.46f, fmaf(ca, cb[i].x, -sa * cb[i].y), 0.54f);
-        const float sgn = ((HALF - 1 - i) & 1) ? -1.0f : 1.0f;
-        const float w = sgn * win * (pre[i] * suf);
+        const float win = fmaf(sa, cw[i].z, fmaf(ca, cw[i].y, cw[i].x));  // (-1)^n (0.54 + 0.46 cos(pi u / half))
+        const float w = win * (pre[i] * suf);
         suf *= d[i];
         wsum += w;
-        const float2 y = tap(j0 - HALF + i);  // 0-based index (j - 1)
-        acc.x = fmaf(w, y.x, acc.x);
-        acc.y = fmaf(w, y.y, acc.y);
+        acc = fma2(make_float2(w, w), tap(i), acc);
     }
     const float inv = 1.0f / wsum;
     return make_float2(acc.x * inv, acc.y * inv);
 }
 
-// grid: (ceil(K / 32), ceil(M / 64)), kKtThreads threads
+// grid: (ceil(K / 32), ceil(M / 64)), kKtThreads threads.  Lane = frequency
+// row k, warp w produces pulses m_a + w + 8 i.  Positions: x = fbar (m + 1) =
+// (m + 1) + e, e = (fbar - 1)(m + 1); per thread e is split once in FP64 at
+// its first pulse into an integer and a fraction, and advanced in FP32 by
+// 8 (fbar - 1) per output (|8 i (fbar - 1)| < 0.3 over a tile at the BASELINE
+// radars: ~1e-8 absolute error in frac, where x itself in FP32 would carry 6e-5).
 template <int HALF>
 __global__ void __launch_bounds__(kKtThreads) keystone_tiled_kernel(KeystoneArgs a) {
-    constexpr int NTAP = 2 * HALF;
+    constexpr int NTAP = 2 * HALF, NW = kKtThreads / 32;
     __shared__ float2 s_in[kKtSpan][kKtRows];
-    __shared__ float2 s_cs[NTAP];  // (cos, sin)(pi n / HALF), n = HALF - 1 - i
-    __shared__ int s_lo, s_n;
+    __shared__ float3 s_cw[NTAP];
+    __shared__ int s_lo, s_n, s_clamp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k = blockIdx.x * kKtRows + lane;
     const bool live = k < a.K;
     const int m_a = blockIdx.y * kKtTile, m_b = min(a.M, m_a + kKtTile);
     const double fk = a.delta_f * static_cast<double>(k < a.K / 2 ? k : k - a.K);
     const double fbar = a.fc / (fk + a.fc);
+    const double dlt = fbar - 1.0;  // exact (Sterbenz)
     if (threadIdx.x < NTAP) {
+        const int n = HALF - 1 - static_cast<int>(threadIdx.x);
         float sn, cs;
-        sincospif(static_cast<float>(HALF - 1 - static_cast<int>(threadIdx.x)) / static_cast<float>(HALF), &sn, &cs);
-        s_cs[threadIdx.x] = make_float2(cs, sn);
+        sincospif(static_cast<float>(n) / static_cast<float>(HALF), &sn, &cs);
+        const float sg = (n & 1) ? -1.0f : 1.0f;
+        s_cw[threadIdx.x] = make_float3(0.54f * sg, 0.46f * sg * cs, -0.46f * sg * sn);
     }
     if (warp == 0) {
-        // the tile's input pulses: union over its rows of the tap windows, clamped
+        // the tile's input pulses: union over its rows of the tap windows (one
+        // pulse of margin on each side for the FP32 position advance)
         int lo = 0x7fffffff, hi = -0x7fffffff;
         if (live) {
-            lo = static_cast<int>(llround(fbar * static_cast<double>(m_a + 1))) - HALF;
-            hi = static_cast<int>(llround(fbar * static_cast<double>(m_b))) + HALF - 1;
+            lo = static_cast<int>(llround(fbar * static_cast<double>(m_a + 1))) - HALF - 1;
+            hi = static_cast<int>(llround(fbar * static_cast<double>(m_b))) + HALF;
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
         if (lane == 0) {
+            s_clamp = lo < 0 || hi > a.M - 1;
             lo = min(max(lo, 0), a.M - 1);
             hi = min(max(hi, 0), a.M - 1);
             s_lo = lo;
@@ -524,22 +540,38 @@ __global__ void __launch_bounds__(kKtThreads) keystone_tiled_kernel(KeystoneArgs
     }
     __syncthreads();
     const int idx_lo = s_lo, n = s_n;
+    const bool clamp = s_clamp;
     const float2* __restrict__ col = a.in + (live ? k : 0);
     const size_t K = static_cast<size_t>(a.K);
-    float2 cb[NTAP];
+    float3 cw[NTAP];
 #pragma unroll
-    for (int i = 0; i < NTAP; ++i) cb[i] = s_cs[i];
-    if (n <= kKtSpan) {
-        for (int i = warp; i < n; i += kKtThreads / 32)
+    for (int i = 0; i < NTAP; ++i) cw[i] = s_cw[i];
+    const bool staged = n <= kKtSpan;
+    if (staged) {
+        for (int i = warp; i < n; i += NW)
             s_in[i][lane] = live ? col[static_cast<size_t>(idx_lo + i) * K] : make_float2(0.f, 0.f);
         __syncthreads();
-        if (!live) return;
-        for (int m = m_a + warp; m < m_b; m += kKtThreads / 32)
-            a.out[k + K * static_cast<size_t>(m)] = keystone_point<HALF, true>(a, s_in, col, cb, fbar, m, idx_lo, lane);
-    } else {
-        if (!live) return;
-        for (int m = m_a + warp; m < m_b; m += kKtThreads / 32)
-            a.out[k + K * static_cast<size_t>(m)] = keystone_point<HALF, false>(a, s_in, col, cb, fbar, m, 0, lane);
+    }
+    if (!live) return;
+    const int m_first = m_a + warp;
+    const double e0 = dlt * static_cast<double>(m_first + 1);
+    const double ea = floor(e0);
+    const int jbase = m_first + 1 + static_cast<int>(ea);
+    const float e0f = static_cast<float>(e0 - ea);
+    const float step = static_cast<float>(dlt * NW);
+    for (int it = 0, m = m_first; m < m_b; ++it, m += NW) {
+        const float ef = fmaf(step, static_cast<float>(it), e0f);
+        const float n1 = floorf(ef + 0.5f);
+        const int j0 = jbase + NW * it + static_cast<int>(n1);
+        const float fr = ef - n1;
+        float2 r;
+        if (staged && !clamp)
+            r = keystone_point<HALF, true, false>(a, s_in, col, cw, j0, fr, idx_lo, lane);
+        else if (staged)
+            r = keystone_point<HALF, true, true>(a, s_in, col, cw, j0, fr, idx_lo, lane);
+        else
+            r = keystone_point<HALF, false, true>(a, s_in, col, cw, j0, fr, 0, lane);
+        a.out[k + K * static_cast<size_t>(m)] = r;
     }
 }
 

@@ -28,7 +28,6 @@
 
 #include "../../include/ltci_cuda.h"
 #include "coarse.cuh"
-#include "coarse2k.cuh"
 #include "cube_io.hpp"
 #include "fine_fft.cuh"
 #include "fine_tc.cuh"
@@ -446,29 +445,8 @@ void launch_coarse_k(const CoarseArgs& a, cudaStream_t st) {
     CK(cudaGetLastError());
 }
 
-// K = 2048, complex64 output (C1, C3): the specialised K1 (coarse2k.cuh);
-// LTCI_COARSE_GENERIC=1 selects the generic kernel for A/B runs
-bool coarse2k_selected() {
-    static const bool generic = [] {
-        const char* env = std::getenv("LTCI_COARSE_GENERIC");
-        return env && std::atoi(env) != 0;
-    }();
-    return !generic;
-}
-
-void launch_coarse2k(const CoarseArgs& a, cudaStream_t st) {
-    ensure_smem_attr(reinterpret_cast<const void*>(coarse2k_kernel), static_cast<int>(coarse2k_smem_bytes()));
-    dim3 grid(a.M / k2kPG, a.c_count);
-    coarse2k_kernel<<<grid, k2kThreads, coarse2k_smem_bytes(), st>>>(a);
-    CK(cudaGetLastError());
-}
-
 template <int OUT16>
 void launch_coarse_out(const CoarseArgs& a, cudaStream_t st) {
-    if (!OUT16 && a.K == 2048 && a.M >= k2kPG && coarse2k_selected()) {
-        launch_coarse2k(a, st);
-        return;
-    }
     switch (a.K) {
         case 16: launch_coarse_k<16, OUT16>(a, st); break;
         case 32: launch_coarse_k<32, OUT16>(a, st); break;

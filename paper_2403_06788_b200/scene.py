@@ -5,8 +5,8 @@ numpy port of
   synthesize_cube    proj/src/signal_model.cpp:37-56
   add_noise          proj/src/signal_model.cpp:58-65
 so that bench.py and the tests can build the BASELINE workloads on any box
-without the reference.  tests/test_scene.py pins it to the reference's own
-generator (oracle/_ref) sample by sample.
+without the reference.  tests/test_oracle.py::test_scene_generator_matches_reference
+pins it to the reference's own generator (oracle/_ref) sample by sample.
 """
 from __future__ import annotations
 

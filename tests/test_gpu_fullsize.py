@@ -2,7 +2,8 @@
 
 Every config is run end to end on the GPU at its BASELINE shape (C2 on a
 1x1 coarse slice, as in bench.py: one full C2 step is ~1.5 h of tensor work)
-and checked by properties that do not need a full-size CPU run:
+and checked by properties that do not need a full-size CPU run (K1, the
+coarse stage, is also checked against the oracle at every row and pulse):
   * the two independent fine-stage formulations (tcgen05 3-term contraction,
     CUDA-core chirp + FFT) agree: per-range-cell peaks (indices identical
     except ties), candidates (identical except near-threshold), argmax;
@@ -80,7 +81,30 @@ def test_c2_full_size_coarse_slice():
     gamma = detection_threshold(w.params, w.sigma2, 1e-6)
     # M = 2048: the tcgen05 contraction and the radix-2-split CUDA-core FFT
     # (fine_fft_tm2k_kernel) against each other and the oracle
-    _cross_and_oracle(w, x, gamma, samples=3, seed=2)
+    _cross_and_oracle(w, x, gamma, samples=8, seed=2)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_coarse_stage_every_row_full_shapes(cfg):
+    """K1 alone at every BASELINE shape (K = 1024, 2048, 4096; GRFT and KT
+    ramps): the mgift output of two coarse cells -- the grid's first and a
+    middle one -- against the FP64 oracle at EVERY range bin and pulse, so a
+    K1 defect cannot hide between the sampled rows of the end-to-end checks."""
+    import oracle as O
+    from paper_2403_06788_b200 import mgift
+    w = config(cfg)
+    p, s = w.params, w.space
+    x = scene.to_complex64_roundtrip(w.cube())
+    if w.variant == 0:
+        mids = [[g.value(0) for g in s.coarse], [g.value(g.count // 2) for g in s.coarse]]
+    else:
+        g2 = s.coarse[1]
+        mids = [[float(w.amb.q_min), g2.value(0)], [float((w.amb.q_min + w.amb.q_max) // 2), g2.value(g2.count // 2)]]
+    for ct in mids:
+        got = mgift(x, p, ct, w.variant)
+        ref = O.port_mgift(x, p, ct, w.variant)
+        err = np.abs(got - ref).max() / np.abs(ref).max()
+        assert err < 2e-5, (ct, err)
 
 
 def test_c3_full_size_kt():
