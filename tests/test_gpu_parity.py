@@ -204,6 +204,30 @@ def test_ds_grft_random_spaces_vs_port():
 
 
 # --------------------------------------------------------------- edges ---
+@pytest.mark.parametrize("M,K,ratio,vb,ab", [(4, 8192, 4.0, 30.0, 8.0), (2048, 16, 8.0, 2.0, 0.2),
+                                            (4, 16, 2.0, 30.0, 8.0)])
+def test_extreme_shapes_vs_port(M, K, ratio, vb, ab):
+    """The supported corners (K = 8192 with M = 4, M = 2048 with K = 16, the
+    4 x 16 minimum): DS-GRFT and DS-KT-MFP dense maps against the oracle."""
+    from paper_2403_06788_b200.model import build_dual_scale
+    p = RadarParams.create(ratio * 100e6, 100e6, 50e6, 2000.0, M, K)
+    s = build_dual_scale(p, 2, [Bounds(-vb, vb), Bounds(-ab, ab)], [0.5, 0.5], RangeRoi(0, K - 1))
+    x = scene.to_complex64_roundtrip(
+        scene.add_noise(scene.synthesize_cube(p, [(0.3, [K / 3 * p.delta_R(), 0.4 * vb, 0.2 * ab])]), 1.0 / K, 7 * K + M))
+    opt = DetectorOptions(retain_threshold=0.5, keep_dense=True)
+    gm = ds_grft(x, p, s, opt)
+    rm = O.port_ds(x, p, s, opt)
+    assert gm.counters == rm.counters
+    assert max_rel(gm.dense, rm.dense) <= TOL
+    check_candidates(gm.cand_index, gm.cand_value, rm.cand_index, rm.cand_value, 0.5)
+    check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
+    amb = build_ambiguity(p, Bounds(-1.6 * p.Va(), 1.6 * p.Va()))
+    gk = ds_kt_mfp(x, p, amb, s, opt)
+    rk = O.port_ds(x, p, s, opt, 1, amb)
+    assert max_rel(gk.dense, rk.dense) <= TOL
+    check_peaks(gk.peak_index, gk.peak_value, rk.peak_index, rk.peak_value, value_at=lambda i: rk.dense[i])
+
+
 def test_zero_cube_and_default_retain():
     p = RadarParams.create(8e8, 100e6, 50e6, 2000.0, 32, 64)
     s = baseline_space(p, [(-40.0, 40.0), (-15.0, 15.0)])
