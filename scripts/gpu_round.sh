@@ -1,7 +1,9 @@
 # Round measurement on one B200: smoke, full GPU suite, bench lines for every config (+ reference arm),
-# side benchmarks (fd_grft, run_pd, cube-file wire path, one-shot call latency), the C1 launch list and
-# ncu --set full captures of the top kernels.  Outputs land in gpurun_out/ (copied to profiles/ by hand).
+# side benchmarks (fd_grft, run_pd, cube-file wire path, one-shot call latency), launch lists and
+# ncu --set full captures of the top kernels.  ncu reports stay in /tmp/ncu on the box (gpurun copies
+# back at most 64 MiB); their headline metrics and per-opcode stall attribution come back as text.
 set -x
+mkdir -p /tmp/ncu
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1
 python bench.py > gpurun_out/bench_c1.log 2>&1
@@ -16,7 +18,9 @@ python scripts/bench_io.py > gpurun_out/side_io.log 2>&1
 python scripts/time_calls.py > gpurun_out/side_calls.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv python scripts/profile_step.py --config 1 > gpurun_out/ncu_launch_c1.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python scripts/profile_step.py --config 3 > gpurun_out/ncu_launch_c3.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"fine_fft_tm|coarse_rm" -c 2 -o gpurun_out/ncu_c1 python scripts/profile_step.py --config 1 > gpurun_out/ncu_c1.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"range_fft|keystone_tiled|fine_fft_tm" -c 3 -o gpurun_out/ncu_c3 python scripts/profile_step.py --config 3 > gpurun_out/ncu_c3.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"fine_fft_tm" -c 1 -o gpurun_out/ncu_c0 python scripts/profile_step.py --config 0 > gpurun_out/ncu_c0.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"fine_fft_tm" -c 1 -o gpurun_out/ncu_c4 python scripts/profile_step.py --config 4 > gpurun_out/ncu_c4.log 2>&1
+for spec in "c1:1:fine_fft_tm|coarse:2" "c3:3:range_fft|keystone_tiled|fine_fft_tm|coarse:4" "c0:0:fine_fft_tm:1" "c4:4:fine_fft_tm:1"; do
+  IFS=: read name cfg regex count <<< "$spec"
+  ncu --set full --import-source on --clock-control none -k regex:"$regex" -c $count -o /tmp/ncu/$name \
+      python scripts/profile_step.py --config $cfg > gpurun_out/ncu_$name.log 2>&1
+  python scripts/ncu_brief.py /tmp/ncu/$name.ncu-rep > gpurun_out/ncu_${name}_brief.txt 2>&1
+done
