@@ -506,6 +506,7 @@ def main():
     # result() D2H: count + R peak slots (16 B) + 24 B per retained candidate (u64 index, complex128)
     res_bytes = lambda m: 8 + 16 * n_rows + 24 * int(m.cand_index.size)  # noqa: E731
     e2e_lanes = n_lanes
+    e2e_steps = args.steps
     if ws == 1:
         # one process streams the job's CPIs step after step through the public API; the
         # lanes keep two in flight (CPI i+1 uploads and runs while CPI i's result drains),
@@ -516,7 +517,11 @@ def main():
             lane_engs.append(Engine(p, s, w.variant, w.amb, opt, row_begin=lo, row_end=hi, coarse_begin=c_lo,
                                     coarse_end=c_hi))
             lane_streams.append(torch.cuda.Stream(dev))
-        items = [(i, k) for i in range(args.warmup + args.steps) for k in range(len(hosts))]
+        # at least ~0.25 s of steps (C0's 0.3 ms steps would otherwise time 1.5 ms of host
+        # calls, at the mercy of scheduler jitter); the line reports per-step averages
+        step_s = ms_max / args.steps * 1e-3
+        e2e_steps = int(min(2000, max(args.steps, np.ceil(0.25 / max(step_s, 1e-6)))))
+        items = [(i, k) for i in range(args.warmup + e2e_steps) for k in range(len(hosts))]
         pending = [None] * e2e_lanes
         t0 = None
         for j, (i, k) in enumerate(items):
@@ -537,8 +542,8 @@ def main():
         for ln in range(e2e_lanes):
             if pending[ln] is not None:
                 d2h += res_bytes(lane_engs[ln].result(lane_streams[ln].cuda_stream))
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        d2h //= args.steps
+        e2e_ms.append((time.perf_counter() - t0) * 1e3 * args.steps / e2e_steps)  # scaled to args.steps steps
+        d2h //= e2e_steps
     else:
         for i in range(args.warmup + args.steps):
             torch.cuda.synchronize(dev)
@@ -682,7 +687,7 @@ def main():
             "roofline": roof,
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": int(cube.size * 16 * len(cubes)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": float(e2e_t.item()) / args.steps,
-                    "lanes": e2e_lanes,
+                    "lanes": e2e_lanes, "steps": e2e_steps if ws == 1 else args.steps,
                     "pipeline": "public API (Engine.run_host_ptr from pinned f64 + result()), CPIs streamed over "
                                 f"{e2e_lanes} engine lanes" if ws == 1 else "per step: upload, run, result, gather"},
             "gpu_launches": int(launches) * args.steps,

@@ -64,6 +64,21 @@ def load():
     if not os.path.exists(LIB_PATH):
         raise OSError(f"{LIB_PATH} not built; run __graft_entry__.build()")
     lib = C.CDLL(LIB_PATH)
+    if os.environ.get("LTCI_LIB_PATH"):
+        # A/B experiments may load an older build: bind what it exports
+        class _Tolerant:
+            def __init__(self, real):
+                object.__setattr__(self, "_real", real)
+
+            def __getattr__(self, name):
+                try:
+                    return getattr(self._real, name)
+                except AttributeError:
+                    return C.CFUNCTYPE(C.c_int)()  # placeholder; calling it is an error
+
+            def __setattr__(self, name, value):
+                setattr(self._real, name, value)
+        lib = _Tolerant(lib)
     P = C.POINTER
     vp = C.c_void_p
     lib.ltci_cuda_ds_grft.argtypes = [vp, P(A.CRadar), P(A.CDualSpace), P(A.COptions), P(A.PMap)]

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <set>
 #include <mutex>
@@ -356,17 +357,21 @@ void radix_plan(int K, int* radix, int* npass) {
     *npass = n;
 }
 
-// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: set it
-// once per (kernel, device), so one process may drive engines on several GPUs
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: raised
+// per (kernel, device) whenever a launch needs more than was set before (a
+// plan with a larger shared footprint -- e.g. K = 16 at M = 2048 on the fp16
+// coarse path -- must not inherit a smaller earlier setting), so one process
+// may drive engines of any shape on several GPUs
 void ensure_smem_attr(const void* kern, int bytes) {
     static std::mutex mu;
-    static std::set<std::pair<const void*, int>> done;
+    static std::map<std::pair<const void*, int>, int> set_to;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    if (done.count({kern, dev})) return;
+    auto it = set_to.find({kern, dev});
+    if (it != set_to.end() && it->second >= bytes) return;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    done.insert({kern, dev});
+    set_to[{kern, dev}] = bytes;
 }
 
 int coarse_pg(int K, int M) { return coarse_pg_for(K, M); }
@@ -439,7 +444,7 @@ template <int K, int OUT16>
 void launch_coarse_k(const CoarseArgs& a, cudaStream_t st) {
     auto kern = coarse_rm_kernel<K, OUT16>;
     const size_t smem = coarse_smem_bytes(K, a.M, OUT16);
-    ensure_smem_attr(reinterpret_cast<const void*>(kern), 160 * 1024);
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(std::max<size_t>(smem, 160 * 1024)));
     dim3 grid(a.M / coarse_pg_for(K, a.M, OUT16), a.c_count);
     kern<<<grid, coarse_threads<OUT16>(), smem, st>>>(a);
     CK(cudaGetLastError());
