@@ -697,10 +697,13 @@ template <typename T>
 struct HostBuf {
     T* p = nullptr;
     size_t n = 0;
+    // portable: pinned (and, with cudaHostAllocMapped, mapped) for every device's
+    // context, so one process may drive engines on several GPUs
     void ensure(size_t count, unsigned flags = cudaHostAllocDefault) {
         if (count <= n) return;
         release();
-        CK(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), flags));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T),
+                         flags | cudaHostAllocPortable));
         n = count;
     }
     void release() {
