@@ -166,13 +166,26 @@ def n_coarse_cells(w) -> int:
     return int(np.prod([g.count for g in s.coarse])) if w.variant == 0 else w.amb.count() * s.coarse[1].count
 
 
+# coarse-stage (K1, plus K0/K4 for configs[3]) time relative to the fine stage,
+# measured on one B200: C0 0.065, C1 0.021, C3 0.022 (profiles/r02_bench_c*.json)
+COARSE_OVER_FINE = 0.03
+
+
 def plan_shard(w, ws: int, requested: str) -> str:
-    """The job's partition across ``ws`` ranks (the same answer in both arms)."""
+    """The job's partition across ``ws`` ranks (the same answer in both arms).
+    auto: the partition with the smaller busiest-rank time -- coarse-cell
+    shards pay ceil(C / ws) whole cells on the busiest rank, range-cell shards
+    split the fine stage evenly but repeat the coarse stage on every rank."""
     if w.cpis > 1:
         return "cpis"
-    if requested == "auto":
-        return "coarse" if n_coarse_cells(w) >= ws else "rows"
-    return requested
+    if requested != "auto":
+        return requested
+    C, R = n_coarse_cells(w), w.space.roi.count()
+    if ws == 1 or C < ws:
+        return "coarse" if C >= ws else "rows"
+    coarse_cost = (1.0 + COARSE_OVER_FINE) * (-(-C // ws)) / C
+    rows_cost = (-(-R // ws)) / R + COARSE_OVER_FINE
+    return "coarse" if coarse_cost <= rows_cost else "rows"
 
 
 def front_of(args) -> str:
