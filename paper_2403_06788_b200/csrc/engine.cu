@@ -34,6 +34,8 @@
 #include "fine_tc.cuh"
 #include "fd_grft.cuh"
 #include "range_fft.cuh"
+#include "fine_launch.hpp"
+#include "launch_util.hpp"
 
 using namespace ltcib;
 
@@ -357,23 +359,6 @@ void radix_plan(int K, int* radix, int* npass) {
     *npass = n;
 }
 
-// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: raised
-// per (kernel, device) whenever a launch needs more than was set before (a
-// plan with a larger shared footprint -- e.g. K = 16 at M = 2048 on the fp16
-// coarse path -- must not inherit a smaller earlier setting), so one process
-// may drive engines of any shape on several GPUs
-void ensure_smem_attr(const void* kern, int bytes) {
-    static std::mutex mu;
-    static std::map<std::pair<const void*, int>, int> set_to;
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = set_to.find({kern, dev});
-    if (it != set_to.end() && it->second >= bytes) return;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    set_to[{kern, dev}] = bytes;
-}
-
 int coarse_pg(int K, int M) { return coarse_pg_for(K, M); }
 
 // K4 launch: the tiled kernel for 2..16 taps (HALF = taps / 2 <= 8), the
@@ -425,19 +410,22 @@ void preload_module() {
         cudaGetLastError();
         return;
     }
-    cudaFunction_t anchor = nullptr;
-    if (cudaGetFuncBySymbol(&anchor, reinterpret_cast<const void*>(module_anchor_kernel)) != cudaSuccess) {
-        cudaGetLastError();
-        return;
+    // this translation unit's module and the fine-kernel one (fine_launch.cu)
+    for (const void* sym : {reinterpret_cast<const void*>(module_anchor_kernel), ltcib::fine_module_anchor()}) {
+        cudaFunction_t anchor = nullptr;
+        if (cudaGetFuncBySymbol(&anchor, sym) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        CUmodule mod = nullptr;
+        unsigned int n = 0;
+        if (reinterpret_cast<GetModule>(p_mod)(&mod, reinterpret_cast<CUfunction>(anchor)) != CUDA_SUCCESS ||
+            reinterpret_cast<Count>(p_cnt)(&n, mod) != CUDA_SUCCESS || n == 0)
+            continue;
+        std::vector<CUfunction> fns(n);
+        if (reinterpret_cast<Enumerate>(p_enum)(fns.data(), n, mod) != CUDA_SUCCESS) continue;
+        for (CUfunction f : fns) reinterpret_cast<Load>(p_load)(f);
     }
-    CUmodule mod = nullptr;
-    unsigned int n = 0;
-    if (reinterpret_cast<GetModule>(p_mod)(&mod, reinterpret_cast<CUfunction>(anchor)) != CUDA_SUCCESS ||
-        reinterpret_cast<Count>(p_cnt)(&n, mod) != CUDA_SUCCESS || n == 0)
-        return;
-    std::vector<CUfunction> fns(n);
-    if (reinterpret_cast<Enumerate>(p_enum)(fns.data(), n, mod) != CUDA_SUCCESS) return;
-    for (CUfunction f : fns) reinterpret_cast<Load>(p_load)(f);
 }
 
 template <int K, int OUT16>
@@ -578,97 +566,6 @@ void launch_tc_terms(const TcArgs& a, const CUtensorMap& hi, const CUtensorMap& 
     const int grid = static_cast<int>(std::min<long long>(tiles, sms));  // persistent: one CTA per SM
     kern<<<grid, TC_THREADS, smem, st>>>(a, hi, lo);
     CK(cudaGetLastError());
-}
-
-// Doppler-window blocks: the smallest NB in {3, 6} with every needed bin in the
-// first or last NB 32-bin blocks, else 0 (any window, e.g. DS-KT-MFP's full axis)
-inline int fine_window_nb(const FineArgs& a, int Q, int G) {
-    const int nbp = a.kA >= 0 ? a.kA / Q + 1 : 0;
-    const int nbn = a.kB <= Q * G - 1 ? G - a.kB / Q : 0;
-    const int nb = std::max(nbp, nbn);
-    if (std::getenv("LTCI_FINE_NOPRUNE")) return 0;
-    return nb <= 3 ? 3 : nb <= 6 ? 6 : 0;
-}
-
-template <int Q, int G, bool DENSE, int NB>
-void launch_fine_tm_nb(const FineArgs& a, cudaStream_t st) {
-    const size_t smem = fine_tm_smem_floats2<Q, G>() * sizeof(float2);
-    auto kern = fine_fft_tm_kernel<Q, G, DENSE, NB>;
-    ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
-    constexpr int rows_per_block = fine_tm_warps<Q, G>() * (32 / G);
-    const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
-    kern<<<dim3(blocks, a.n_split), fine_tm_warps<Q, G>() * 32, smem, st>>>(a);
-    CK(cudaGetLastError());
-}
-
-template <int Q, int G, bool DENSE>
-void launch_fine_tm(const FineArgs& a, cudaStream_t st) {
-    if constexpr (G >= 8) {
-        const int nb = 2 * fine_window_nb(a, Q, G) <= G ? fine_window_nb(a, Q, G) : 0;
-        if (nb == 3) return launch_fine_tm_nb<Q, G, DENSE, 3>(a, st);
-        if (nb == 6) return launch_fine_tm_nb<Q, G, DENSE, 6>(a, st);
-    }
-    launch_fine_tm_nb<Q, G, DENSE, 0>(a, st);
-}
-
-template <int Q, int G, bool DENSE>
-void launch_fine_qg(const FineArgs& a, cudaStream_t st) {
-    if constexpr (Q == 32 && (G == 32 || G == 16 || G == 8)) {
-        if (!std::getenv("LTCI_FINE_TM_OFF")) {  // TMEM-resident row variant (M = 1024, 512, 256)
-            launch_fine_tm<Q, G, DENSE>(a, st);
-            return;
-        }
-    }
-    if (a.n_split != 1) fail(LTCI_RUNTIME_ERROR, "ltci_cuda: fine-axis split on a kernel without it");
-    constexpr int rows_per_block = (kFineThreads / 32) * (32 / G);
-    const size_t smem = fine_smem_floats2<Q, G>() * sizeof(float2);
-    auto kern = fine_fft_kernel<Q, G, DENSE>;
-    ensure_smem_attr(reinterpret_cast<const void*>(kern), 200 * 1024);
-    const int blocks = (a.rows + rows_per_block - 1) / rows_per_block;
-    kern<<<blocks, kFineThreads, smem, st>>>(a);
-    CK(cudaGetLastError());
-}
-
-// M = 2048 (fine_fft_tm2k_kernel): NB over the half-length (1024-bin) axes of
-// the even and odd output bins; 0 = window too wide for the kernel
-inline int tm2k_nb(int kA, int kB) {
-    const int nbp = kA >= 0 ? (kA / 2) / 32 + 1 : 0;
-    const int nbn = kB <= 2047 ? 32 - ((kB - 1) / 2) / 32 : 0;
-    const int nb = std::max(nbp, nbn);
-    return nb <= 3 ? 3 : nb <= 6 ? 6 : 0;
-}
-
-template <bool DENSE, int NB>
-void launch_fine_tm2k_nb(const FineArgs& a, cudaStream_t st) {
-    auto kern = fine_fft_tm2k_kernel<DENSE, NB>;
-    const int smem = fine_tm2k_smem_bytes();
-    ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
-    const int blocks = (a.rows + kTm2kWarps - 1) / kTm2kWarps;
-    kern<<<blocks, kTm2kWarps * 32, smem, st>>>(a);
-    CK(cudaGetLastError());
-}
-
-template <bool DENSE>
-void launch_fine_m(const FineArgs& a, int M, cudaStream_t st) {
-    if (M == 2048) {
-        const int nb = tm2k_nb(a.kA, a.kB);
-        if (nb == 3) return launch_fine_tm2k_nb<DENSE, 3>(a, st);
-        if (nb == 6) return launch_fine_tm2k_nb<DENSE, 6>(a, st);
-        fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: CUDA-core fine path at M = 2048 needs a Doppler window of "
-                                    "at most 12 x 64 bins (use the tcgen05 path)");
-    }
-    switch (M) {
-        case 4: launch_fine_qg<4, 1, DENSE>(a, st); break;
-        case 8: launch_fine_qg<8, 1, DENSE>(a, st); break;
-        case 16: launch_fine_qg<16, 1, DENSE>(a, st); break;
-        case 32: launch_fine_qg<32, 1, DENSE>(a, st); break;
-        case 64: launch_fine_qg<32, 2, DENSE>(a, st); break;
-        case 128: launch_fine_qg<32, 4, DENSE>(a, st); break;
-        case 256: launch_fine_qg<32, 8, DENSE>(a, st); break;
-        case 512: launch_fine_qg<32, 16, DENSE>(a, st); break;
-        case 1024: launch_fine_qg<32, 32, DENSE>(a, st); break;
-        default: fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: unsupported M");
-    }
 }
 
 // --------------------------------------------------------------- engine ---
@@ -1052,9 +949,9 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
             ++e->launches;
         } else {
             if (pl.keep_dense)
-                launch_fine_m<true>(fa, M, st);
+                launch_fine_m(fa, M, true, st);
             else
-                launch_fine_m<false>(fa, M, st);
+                launch_fine_m(fa, M, false, st);
             ++e->launches;
         }
         if (evc >= 0) {
@@ -1986,7 +1883,7 @@ int ltci_cuda_gft(const double* rows, const ltci_radar* p, const double* fine_hi
         fa.n_split = 1;
         fa.chunk = 1;
         fa.retain2 = INFINITY;
-        launch_fine_m<true>(fa, M, nullptr);
+        launch_fine_m(fa, M, true, nullptr);
         std::vector<float2> hd(static_cast<size_t>(R) * M);
         CK(cudaMemcpy(hd.data(), dense.p, hd.size() * sizeof(float2), cudaMemcpyDeviceToHost));
         // dense[r*M + j] -> map data[r + R*j] with the recentring twiddle
