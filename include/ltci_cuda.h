@@ -268,6 +268,13 @@ int ltci_engine_set_timing(ltci_engine *e, int enable);
 /* Fine-stage formulation this engine runs (LTCI_FINE_FFT_CUDA_CORE or
  * LTCI_FINE_TC_DENSE / LTCI_FINE_TC_FAST) and its fp16 split terms (0 for FFT). */
 int ltci_engine_fine_path(ltci_engine *e, int32_t *path, int32_t *terms);
+/* Coarse-stage (mgift, proj/src/transforms.cpp:134-173) formulation this engine
+ * runs: LTCI_COARSE_TRANSFORM = one K-point transform per (coarse cell, pulse),
+ * LTCI_COARSE_GATHER = interpolation of 2x-oversampled range profiles tabulated
+ * once per pulse (the default before the FP32 fine path; LTCI_COARSE=transform
+ * or =gather in the environment forces one). */
+enum { LTCI_COARSE_TRANSFORM = 0, LTCI_COARSE_GATHER = 1 };
+int ltci_engine_coarse_path(ltci_engine *e, int32_t *path);
 /* hypotheses (cells) and integrations covered by this engine's row slice */
 int ltci_engine_work(ltci_engine *e, uint64_t *hypotheses, uint64_t *integrations);
 /* extension: restrict the engine to coarse cells [c_begin, c_end) of the plan

@@ -20,7 +20,7 @@ EXPORTS = (
     "ltci_cuda_ds_grft", "ltci_cuda_ds_kt_mfp", "ltci_cuda_free_map", "ltci_cuda_keystone", "ltci_cuda_keystone_device", "ltci_cuda_range_fft", "ltci_cuda_range_fft_device", "ltci_engine_run_range_device", "ltci_engine_run_range_host",
     "ltci_cuda_mgift", "ltci_cuda_gft", "ltci_cuda_detection_threshold", "ltci_engine_create",
     "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
-    "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path",
+    "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path", "ltci_engine_coarse_path",
     "ltci_engine_work", "ltci_engine_run_file", "ltci_engine_set_coarse_slice", "ltci_cuda_merge_peaks", "ltci_cuda_fd_grft", "ltci_cuda_extract_detections_single",
     "ltci_cuda_extract_detections", "ltci_cuda_cube_file_info", "ltci_cuda_cube_file_read",
     "ltci_cuda_cube_file_write", "ltci_cuda_synthesize", "ltci_cuda_add_noise", "ltci_cuda_run_pd", "ltci_cuda_measure_fp32_peak", "ltci_cuda_pool_idle", "ltci_cuda_last_error", "ltci_cuda_version",
@@ -108,6 +108,7 @@ def load():
     lib.ltci_engine_set_timing.argtypes = [vp, C.c_int]
     lib.ltci_engine_work.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     lib.ltci_engine_fine_path.argtypes = [vp, P(C.c_int32), P(C.c_int32)]
+    lib.ltci_engine_coarse_path.argtypes = [vp, P(C.c_int32)]
     lib.ltci_cuda_measure_fp32_peak.argtypes = [C.c_int, P(C.c_double)]
     lib.ltci_cuda_pool_idle.argtypes = [C.c_int, P(C.c_int64), P(C.c_int64)]
     lib.ltci_cuda_extract_detections.argtypes = [P(A.CDetectionMap), P(A.CDualSpace), P(A.CAmbiguity), C.c_double,

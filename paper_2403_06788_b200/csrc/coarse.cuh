@@ -35,6 +35,7 @@ struct CoarseArgs {
     int R_slice;
     double inv_prf, inv_dR, two_over_lambda, Va;
     double kt_b;             // -(4 pi / c) * delta_f^2 / fc  (times q Va t)
+    const float* deap;       // TAB = 1: per-frequency-row real scale (gather.cuh deapodisation)
     int npass;
     int radix[8];
 };
@@ -224,8 +225,11 @@ __device__ __forceinline__ void coarse_middle_passes(float2* __restrict__ buf, i
 }
 
 // grid: (M / PG, c_count); block coarse_threads<OUT16>(); dynamic smem = coarse_smem_bytes
-template <int K, int OUT16>
-__global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT16>())
+// TAB = 1 builds the oversampled range profiles of gather.cuh with the same
+// passes: "cell" blockIdx.y has cparams (delta in range cells, folding number
+// q, -, -), no preDFM factor, and every frequency row is scaled by deap[k].
+template <int K, int OUT16, int TAB = 0>
+__global__ void __launch_bounds__(coarse_threads<OUT16>(), TAB ? 2 : coarse_min_blocks<OUT16>())
     coarse_rm_kernel(CoarseArgs a) {
     constexpr int NT = coarse_threads<OUT16>();
     constexpr bool SW = coarse_swizzled<K, OUT16>();
@@ -248,7 +252,11 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT
         const double t = static_cast<double>(m + 1) * a.inv_prf;
         const double* cp = a.cparams + 4 * c;
         double s_rm, s_predfm, b = 0.0;
-        if (a.variant == 0) {
+        if constexpr (TAB) {
+            s_rm = 0.0;
+            s_predfm = 0.0;
+            b = a.kt_b * cp[1] * a.Va * t;
+        } else if (a.variant == 0) {
             // poly_from(c, t, 1): sum_p c_p t^p (transforms.cpp:12-22)
             double tp = 1.0, acc = 0.0;
             for (int p = 0; p < a.P; ++p) {
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT
             s_predfm = cp[1] * t * t;
             b = a.kt_b * qva * t;
         }
-        const double delta = s_rm * a.inv_dR;
+        const double delta = TAB ? cp[0] : s_rm * a.inv_dR;
         const double sh = floor(delta + 0.5);
         const double frac = delta - sh;
         long long shl = static_cast<long long>(sh) % K;
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT
                     const float c0 = static_cast<float>((j * sp) & (K - 1)) * kInvK;
                     const float c1 = static_cast<float>((S * sp) & (K - 1)) * kInvK;
                     const float fj = static_cast<float>(j);
-                    if (a.variant == 0) {
+                    if (!TAB && a.variant == 0) {
                         // GRFT: the phase is linear in r on each half (g jumps by -K at r = 8),
                         // so 3 sincos per 16 points: the two half bases and the common step,
                         // then an 8-long power chain per half (fp32 drift ~1e-6 rel).
@@ -341,6 +349,11 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), coarse_min_blocks<OUT
                             float sn, cs;
                             __sincosf(fmaf(6.28318530717958647692f, ti, fmaf(rb * gg, gg, fmaf(ra, gg, pre))), &sn,
                                       &cs);
+                            if constexpr (TAB) {
+                                const float dp = __ldg(a.deap + j + r * S);
+                                cs *= dp;
+                                sn *= dp;
+                            }
                             v[h][r] = cmul(v[h][r], make_float2(cs, sn));
                         }
                     }
@@ -368,7 +381,7 @@ inline size_t coarse_smem_bytes(int K, int M, int out16 = 1) {
 }
 
 // f64 interleaved host layout -> complex64 device cube
-__global__ void f64_to_c64_kernel(const double2* __restrict__ in, float2* __restrict__ out, size_t n) {
+static __global__ void f64_to_c64_kernel(const double2* __restrict__ in, float2* __restrict__ out, size_t n) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const double2 v = in[i];
@@ -388,7 +401,7 @@ struct KeystoneArgs {
     double fc, delta_f;
 };
 
-__global__ void __launch_bounds__(256) keystone_kernel(KeystoneArgs a) {
+static __global__ void __launch_bounds__(256) keystone_kernel(KeystoneArgs a) {
     const size_t total = static_cast<size_t>(a.K) * a.M;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {

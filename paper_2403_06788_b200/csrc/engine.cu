@@ -35,6 +35,7 @@
 #include "fd_grft.cuh"
 #include "range_fft.cuh"
 #include "fine_launch.hpp"
+#include "gather_launch.hpp"
 #include "launch_util.hpp"
 
 using namespace ltcib;
@@ -411,7 +412,8 @@ void preload_module() {
         return;
     }
     // this translation unit's module and the fine-kernel one (fine_launch.cu)
-    for (const void* sym : {reinterpret_cast<const void*>(module_anchor_kernel), ltcib::fine_module_anchor()}) {
+    for (const void* sym : {reinterpret_cast<const void*>(module_anchor_kernel), ltcib::fine_module_anchor(),
+                            ltcib::gather_module_anchor()}) {
         cudaFunction_t anchor = nullptr;
         if (cudaGetFuncBySymbol(&anchor, sym) != cudaSuccess) {
             cudaGetLastError();
@@ -626,6 +628,88 @@ struct Stager {
 
 void ltcib_set_last_error(const char* msg) { g_err = msg ? msg : ""; }
 
+// K1g workspace (gather.cuh): the oversampled range profiles of the current
+// cube, the deapodisation row scales (depend on K only) and the per-batch
+// (cell, pulse) weights.
+struct GatherStage {
+    DevBuf<float2> U;
+    DevBuf<float> deap;
+    DevBuf<float4> W;
+    DevBuf<double> tparams;
+    int deap_K = 0;
+    int tables = 0;
+    unsigned long long cells_per_table = 1;
+    // q: the folding number of each table (KT), one zero for GRFT
+    void init(int K, int M, const std::vector<double>& q, unsigned long long cpt, unsigned long long batch) {
+        tables = static_cast<int>(q.size());
+        cells_per_table = cpt;
+        U.ensure(static_cast<size_t>(tables) * 2 * K * M);
+        W.ensure(static_cast<size_t>(3) * batch * M);
+        if (static_cast<size_t>(K) > deap.n) {
+            deap.ensure(K);
+            deap_K = 0;
+        }
+        std::vector<double> tp(static_cast<size_t>(tables) * 8, 0.0);
+        for (int t = 0; t < tables; ++t) {
+            tp[8 * t + 1] = q[t];       // even fine samples: delta = 0
+            tp[8 * t + 4] = 0.5;        // odd fine samples: delta = 1/2
+            tp[8 * t + 5] = q[t];
+        }
+        tparams.ensure(tp.size());
+        CK(cudaMemcpy(tparams.p, tp.data(), tp.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    // tables of `base.cube` (base: the coarse stage's radar scalars); returns the kernels launched
+    int build(const CoarseArgs& base, cudaStream_t st) {
+        int n = 1;
+        if (deap_K != base.K) {
+            launch_gather_deap(deap.p, base.K, st);
+            deap_K = base.K;
+            ++n;
+        }
+        CoarseArgs ta = base;
+        ta.cparams = tparams.p;
+        ta.X = U.p;
+        ta.c_begin = 0;
+        ta.c_count = 2 * tables;
+        ta.n_base = 0;
+        ta.R_slice = base.K;
+        ta.deap = deap.p;
+        launch_gather_tables(ta, st);
+        return n;
+    }
+    GatherArgs args(const CoarseArgs& base) const {
+        GatherArgs g{};
+        g.U = U.p;
+        g.W = W.p;
+        g.cparams = base.cparams;
+        g.X = base.X;
+        g.cells_per_table = cells_per_table;
+        g.K = base.K;
+        g.M = base.M;
+        g.P = base.P;
+        g.variant = base.variant;
+        g.n_base = base.n_base;
+        g.R_slice = base.R_slice;
+        g.inv_prf = base.inv_prf;
+        g.inv_dR = base.inv_dR;
+        g.two_over_lambda = base.two_over_lambda;
+        g.Va = base.Va;
+        return g;
+    }
+};
+
+// LTCI_COARSE = transform | gather forces the coarse kernel (A/B and tests);
+// otherwise K1g runs whenever the FP32 fine path follows, the shape fits and a
+// table (two transforms per pulse) serves at least four coarse cells.
+bool gather_selected(int K, int M, bool use_tc, unsigned long long cells_per_table) {
+    if (use_tc || !gather_supported(K, M)) return false;
+    if (const char* env = std::getenv("LTCI_COARSE")) {
+        if (!std::strcmp(env, "transform")) return false;
+        if (!std::strcmp(env, "gather")) return true;
+    }
+    return cells_per_table >= 4;
+}
+
 struct ltci_engine {
     Plan pl;
     int device = 0;
@@ -651,6 +735,9 @@ struct ltci_engine {
     DevBuf<float2> htab;
     bool htab_ready = false;
     CUtensorMap tm_hi{}, tm_lo{};
+    // interpolating coarse gather (K1g)
+    bool use_gather = false;
+    GatherStage gs;
     // coarse-cell slice searched by this engine (coarse-cell sharding across GPUs)
     unsigned long long c_lo = 0, c_hi = ~0ull;
     // candidate assembly on the device (radix sort by flat index + recentring)
@@ -775,6 +862,17 @@ void engine_init(ltci_engine* e) {
         e->tm_lo = make_x16_map(e->x16l.p, M, rows_cap);
     } else {
         e->X.ensure(e->batch * per_coarse / sizeof(float2));
+    }
+    {
+        const bool kt = pl.variant == LTCI_VARIANT_KTMFP;
+        const unsigned long long cpt = kt ? pl.coarse_cells / static_cast<unsigned long long>(pl.q_count) : pl.coarse_cells;
+        e->use_gather = gather_selected(pl.rp.K, M, e->use_tc, cpt);
+        if (e->use_gather) {
+            std::vector<double> q(kt ? pl.q_count : 1, 0.0);
+            if (kt)
+                for (int i = 0; i < pl.q_count; ++i) q[i] = static_cast<double>(pl.q_min + i);
+            e->gs.init(pl.rp.K, M, q, cpt, e->batch);
+        }
     }
     const unsigned long long H = pl.coarse_cells * pl.fine_cells * pl.R_slice * pl.D;
     unsigned long long cap0 = 1ull << 22;  // initial candidate buffer (grown by the overflow re-run)
@@ -923,6 +1021,22 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
         ta.htab = e->htab.p;
     }
     const unsigned long long c_end = std::min(e->c_hi, pl.coarse_cells);
+    GatherArgs ga{};
+    if (e->use_gather && e->c_lo < c_end) {
+        // the oversampled profiles of this cube, once per run (counted in coarse_ms)
+        int evt = -1;
+        if (tm && evi + 2 <= static_cast<int>(e->ev.size())) {
+            evt = evi;
+            evi += 2;
+            CK(cudaEventRecord(e->ev[evt], st));
+        }
+        e->launches += e->gs.build(ca, st);
+        if (evt >= 0) {
+            CK(cudaEventRecord(e->ev[evt + 1], st));
+            coarse_ev.push_back({evt, evt + 1});
+        }
+        ga = e->gs.args(ca);
+    }
     for (unsigned long long c0 = e->c_lo; c0 < c_end; c0 += e->batch) {
         const unsigned long long cc = std::min<unsigned long long>(e->batch, c_end - c0);
         ca.c_begin = c0;
@@ -933,8 +1047,14 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
             evi += 4;
             CK(cudaEventRecord(e->ev[evc], st));
         }
-        launch_coarse(ca, pg, st, use_tc);
-        ++e->launches;
+        if (e->use_gather) {
+            ga.c_begin = c0;
+            ga.c_count = static_cast<int>(cc);
+            e->launches += launch_gather_cells(ga, st);
+        } else {
+            launch_coarse(ca, pg, st, use_tc);
+            ++e->launches;
+        }
         if (evc >= 0) CK(cudaEventRecord(e->ev[evc + 1], st));
         fa.c_begin = c0;
         fa.rows = static_cast<int>(cc) * pl.R_slice;
@@ -1801,7 +1921,17 @@ int ltci_cuda_mgift(const double* cube, const ltci_radar* p, const double* ctild
         ca.Va = va_of(*p);
         ca.kt_b = -(4.0 * kPi / kC) * p->delta_f * p->delta_f / p->fc;
         radix_plan(K, ca.radix, &ca.npass);
-        launch_coarse(ca, coarse_pg(K, M), nullptr);
+        GatherStage gs;
+        if (gather_selected(K, M, false, 1)) {  // one cell: only when LTCI_COARSE=gather forces it
+            gs.init(K, M, {variant == LTCI_VARIANT_KTMFP ? cp4[0] : 0.0}, 1, 1);
+            gs.build(ca, nullptr);
+            GatherArgs ga = gs.args(ca);
+            ga.c_begin = 0;
+            ga.c_count = 1;
+            launch_gather_cells(ga, nullptr);
+        } else {
+            launch_coarse(ca, coarse_pg(K, M), nullptr);
+        }
         std::vector<float2> h(n);
         CK(cudaMemcpy(h.data(), X.p, n * sizeof(float2), cudaMemcpyDeviceToHost));
         // X[n][m] -> RangePulseCube data[n + K*m]
@@ -2070,6 +2200,13 @@ int ltci_engine_fine_path(ltci_engine* e, int32_t* path, int32_t* terms) {
         if (!e) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
         if (path) *path = e->use_tc ? (e->tc_terms == 1 ? LTCI_FINE_TC_FAST : LTCI_FINE_TC_DENSE) : LTCI_FINE_FFT_CUDA_CORE;
         if (terms) *terms = e->use_tc ? e->tc_terms : 0;
+    });
+}
+
+int ltci_engine_coarse_path(ltci_engine* e, int32_t* path) {
+    return guarded([&] {
+        if (!e || !path) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        *path = e->use_gather ? LTCI_COARSE_GATHER : LTCI_COARSE_TRANSFORM;
     });
 }
 

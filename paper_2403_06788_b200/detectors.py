@@ -226,6 +226,12 @@ class Engine:
         _lib.raise_for(self._lib.ltci_engine_fine_path(self._h, C.byref(pth), C.byref(t)), self._lib)
         return pth.value, t.value
 
+    def coarse_path(self) -> str:
+        """'gather' (interpolated oversampled profiles, csrc/gather.cuh) or 'transform' (csrc/coarse.cuh)."""
+        pth = C.c_int32()
+        _lib.raise_for(self._lib.ltci_engine_coarse_path(self._h, C.byref(pth)), self._lib)
+        return "gather" if pth.value == 1 else "transform"
+
     def work(self):
         h, i = C.c_uint64(), C.c_uint64()
         _lib.raise_for(self._lib.ltci_engine_work(self._h, C.byref(h), C.byref(i)), self._lib)

@@ -1,0 +1,147 @@
+"""The interpolating coarse gather (K1g, csrc/gather.cuh) against the oracle
+and against the transform kernel K1 (csrc/coarse.cuh) it replaces.
+
+mgift (reference proj/src/transforms.cpp:134-173) through `LTCI_COARSE=gather`
+is held to the same 2e-5 as the transform kernel; whole detector runs with
+the two coarse formulations must agree on every per-range-cell peak."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2403_06788_b200 import AmbiguitySpace, DetectorOptions, ds_grft, ds_kt_mfp, mgift, scene
+from paper_2403_06788_b200.configs import config
+from paper_2403_06788_b200.detectors import Engine, detection_threshold
+from paper_2403_06788_b200.model import Bounds, RadarParams, RangeRoi, build_ambiguity, build_dual_scale
+
+from helpers import TOL, check_candidates, check_peaks, cube, load, max_rel, radar, space
+
+pytestmark = pytest.mark.gpu
+
+KTOL = 2e-5
+
+
+@pytest.fixture
+def gather(monkeypatch):
+    monkeypatch.setenv("LTCI_COARSE", "gather")
+
+
+@pytest.fixture
+def transform(monkeypatch):
+    monkeypatch.setenv("LTCI_COARSE", "transform")
+
+
+def test_mgift_gather_matches_reference_golden(gather):
+    g = load("transforms.npz")
+    p = radar(g)
+    x = cube(g)
+    d = mgift(x, p, [11.7, -4.1]) - g["mgift"]
+    assert np.abs(d).max() / np.abs(g["mgift"]).max() < KTOL
+    d = mgift(x, p, [2.0, 3.3], 1) - g["mgift_kt"]
+    assert np.abs(d).max() / np.abs(g["mgift_kt"]).max() < KTOL
+
+
+@pytest.mark.parametrize("M,K", [(32, 64), (64, 128), (128, 256), (256, 512), (512, 1024), (1024, 2048),
+                                 (256, 4096), (32, 8192)])
+def test_mgift_gather_all_sizes(gather, M, K):
+    """White noise over the whole band (the worst case for the interpolation
+    window), shifts of every size and sign, third order, the keystone variant
+    with a large folding number."""
+    p = RadarParams.create(3e9, 20e6, 18e6, 1000.0, M, K)
+    x = scene.to_complex64_roundtrip(scene.add_noise(np.zeros((M, K), complex), 1.0, M + K))
+    for c, v in (([123.0, -7.5], 0), ([-2711.0, 95.0], 0), ([41.0, 3.0, 0.4], 0), ([0.0], 0), ([3.0, 6.5], 1),
+                 ([-6.0, -11.0], 1)):
+        ref = O.port_mgift(x, p, c, v)
+        got = mgift(x, p, c, v)
+        assert np.abs(got - ref).max() / np.abs(ref).max() < KTOL, (c, v)
+
+
+def test_mgift_gather_point_target(gather):
+    """A single range-compressed point (sinc profile): the gathered peak
+    follows the trajectory to the same accuracy."""
+    M, K = 64, 512
+    p = RadarParams.create(3e9, 25e6, 20e6, 1000.0, M, K)
+    x = scene.to_complex64_roundtrip(scene.synthesize_cube(p, [(1.0, [200.3 * p.delta_R(), 87.0, 2.0])]))
+    for c in ([87.0, 2.0], [-150.0, 5.0]):
+        ref = O.port_mgift(x, p, c, 0)
+        assert np.abs(mgift(x, p, c, 0) - ref).max() / np.abs(ref).max() < KTOL
+
+
+def _run(w, x, gamma, keep_dense=False):
+    e = Engine(w.params, w.space, w.variant, w.amb, DetectorOptions(retain_threshold=gamma, keep_dense=keep_dense))
+    try:
+        e.run_host(x)
+        return e.coarse_path(), e.result()
+    finally:
+        e.close()
+
+
+def test_engine_paths_agree_c0(monkeypatch):
+    """configs[0] through both coarse formulations: same counters, candidates
+    and per-range-cell peaks (values to 1e-4, indices identical except ties)."""
+    g = load("c0.npz")
+    w = config(0)
+    x = cube(g)
+    gamma = float(g["gamma"])
+    monkeypatch.setenv("LTCI_COARSE", "transform")
+    pt, mt = _run(w, x, gamma)
+    monkeypatch.setenv("LTCI_COARSE", "gather")
+    pg, mg = _run(w, x, gamma)
+    assert (pt, pg) == ("transform", "gather")
+    assert mt.counters == mg.counters
+    rel = np.abs(np.abs(mg.peak_value) - np.abs(mt.peak_value)) / np.abs(mt.peak_value)
+    assert rel.max() < 1e-4
+    assert (mg.peak_index != mt.peak_index).sum() <= 3
+    check_candidates(mg.cand_index, mg.cand_value, mt.cand_index, mt.cand_value, gamma)
+    # and the golden itself
+    from test_gpu_parity import _cell_value
+    check_peaks(mg.peak_index, mg.peak_value, g["peak_index"], g["peak_value"],
+                value_at=lambda i: _cell_value(x, w, i))
+
+
+def test_default_is_gather():
+    w = config(0)
+    e = Engine(w.params, w.space, w.variant, w.amb, DetectorOptions(retain_threshold=1e9))
+    try:
+        assert e.coarse_path() == "gather"
+    finally:
+        e.close()
+
+
+def test_small_goldens_gather(gather):
+    """The reference's dense small-case maps (DS-GRFT and DS-KT-MFP, ROI
+    subset, several folding numbers) with the gather forced."""
+    g = load("small_grft.npz")
+    p = radar(g)
+    gm = ds_grft(cube(g), p, space(g, p), DetectorOptions(retain_threshold=float(g["retain"]), keep_dense=True))
+    assert np.abs(gm.dense - g["dense"]).max() / np.abs(g["dense"]).max() <= TOL
+    check_peaks(gm.peak_index, gm.peak_value, g["peak_index"], g["peak_value"], value_at=lambda i: g["dense"][i])
+    g = load("small_kt.npz")
+    p = radar(g)
+    amb = AmbiguitySpace(int(g["amb"][0]), int(g["amb"][1]))
+    gm = ds_kt_mfp(cube(g), p, amb, space(g, p), DetectorOptions(retain_threshold=float(g["retain"]), keep_dense=True))
+    assert np.abs(gm.dense - g["dense"]).max() / np.abs(g["dense"]).max() <= TOL
+    check_peaks(gm.peak_index, gm.peak_value, g["peak_index"], g["peak_value"], value_at=lambda i: g["dense"][i])
+
+
+def test_random_spaces_gather_vs_port(gather):
+    """Reference-built spaces with ROI subsets: dense maps against the port."""
+    rng = np.random.default_rng(11)
+    for K, M, ratio in ((64, 32, 4.0), (128, 32, 8.0), (256, 128, 16.0)):
+        p = RadarParams.create(ratio * 100e6, 100e6, 50e6, 2000.0, M, K)
+        s = build_dual_scale(p, 2, [Bounds(-30.0, 30.0), Bounds(-8.0, 8.0)], [0.5, 0.5],
+                             RangeRoi(int(rng.integers(0, K // 4)), K - 1 - int(rng.integers(0, K // 4))))
+        x = scene.to_complex64_roundtrip(
+            scene.add_noise(scene.synthesize_cube(p, [(0.3, [K / 2 * p.delta_R(), 11.0, 2.5])]), 1.0 / K, K + M))
+        opt = DetectorOptions(retain_threshold=0.5, keep_dense=True)
+        gm = ds_grft(x, p, s, opt)
+        rm = O.port_ds(x, p, s, opt)
+        assert max_rel(gm.dense, rm.dense) <= TOL
+        assert np.abs(gm.dense - rm.dense).max() / np.abs(rm.dense).max() <= TOL
+        check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
+        amb = build_ambiguity(p, Bounds(-1.6 * p.Va(), 1.6 * p.Va()))
+        gk = ds_kt_mfp(x, p, amb, s, opt)
+        rk = O.port_ds(x, p, s, opt, variant=1, amb=amb)
+        assert np.abs(gk.dense - rk.dense).max() / np.abs(rk.dense).max() <= TOL
+        check_peaks(gk.peak_index, gk.peak_value, rk.peak_index, rk.peak_value, value_at=lambda i: rk.dense[i])
