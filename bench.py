@@ -650,8 +650,14 @@ def main():
                                       "fp32_tflops": coarse_fft_flops / (st["coarse_ms"] * 1e-3) / 1e12
                                       if st["coarse_ms"] > 0 else None,
                                       "fp32_algorithmic": "per (coarse cell, pulse): 5 K log2 K FFT + 8 K ramp",
-                                      "note": "exact fractional-delay gather = one K-point transform per "
-                                              "(coarse cell, pulse); issue-bound, see profiles/r01_ncu_c1.json"}})
+                                      "path": eng.coarse_path(),
+                                      "note": ("K1g (gather.cuh): 8-tap interpolation of 2x-oversampled range "
+                                               "profiles tabulated once per pulse (type-2 NUFFT, 1.3e-7 of the "
+                                               "profile maximum); table build + weights + gather are all inside "
+                                               "coarse_ms; fp32_tflops is what the replaced transforms would "
+                                               "have cost, not work done" if eng.coarse_path() == "gather" else
+                                               "K1 (coarse.cuh): one K-point transform per (coarse cell, pulse); "
+                                               "issue-bound, see profiles/r01_ncu_c1.json")}})
         if w.variant == 1:
             # K4 keystone timed over back-to-back calls (one call is ~5 us of
             # traffic, launch latency would dominate a single timing)

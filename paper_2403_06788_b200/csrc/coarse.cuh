@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), TAB ? 2 : coarse_min_
                     const float c0 = static_cast<float>((j * sp) & (K - 1)) * kInvK;
                     const float c1 = static_cast<float>((S * sp) & (K - 1)) * kInvK;
                     const float fj = static_cast<float>(j);
-                    if (!TAB && a.variant == 0) {
+                    if (a.variant == 0) {
                         // GRFT: the phase is linear in r on each half (g jumps by -K at r = 8),
                         // so 3 sincos per 16 points: the two half bases and the common step,
                         // then an 8-long power chain per half (fp32 drift ~1e-6 rel).
@@ -338,6 +338,13 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), TAB ? 2 : coarse_min_
                             if (r < 7) {
                                 w0 = cmul(w0, st);
                                 w8 = cmul(w8, st);
+                            }
+                        }
+                        if constexpr (TAB) {
+#pragma unroll
+                            for (int r = 0; r < 16; ++r) {
+                                const float dp = __ldg(a.deap + j + r * S);
+                                v[h][r] = mul2(v[h][r], make_float2(dp, dp));
                             }
                         }
                     } else {

@@ -639,12 +639,20 @@ struct GatherStage {
     int deap_K = 0;
     int tables = 0;
     unsigned long long cells_per_table = 1;
+    // the weights depend on the plan only: kept for every coarse cell of the
+    // plan when they fit 1 GiB (w_ready after the first run), else per batch
+    bool w_whole = false, w_ready = false;
+    size_t w_plane = 0;
     // q: the folding number of each table (KT), one zero for GRFT
-    void init(int K, int M, const std::vector<double>& q, unsigned long long cpt, unsigned long long batch) {
+    void init(int K, int M, const std::vector<double>& q, unsigned long long cpt, unsigned long long batch,
+              unsigned long long plan_cells) {
         tables = static_cast<int>(q.size());
         cells_per_table = cpt;
         U.ensure(static_cast<size_t>(tables) * 2 * K * M);
-        W.ensure(static_cast<size_t>(3) * batch * M);
+        w_whole = gather_weight_bytes(plan_cells, M) <= (1ull << 30);
+        w_ready = false;
+        w_plane = static_cast<size_t>(w_whole ? plan_cells : batch) * M;
+        W.ensure(3 * w_plane);
         if (static_cast<size_t>(K) > deap.n) {
             deap.ensure(K);
             deap_K = 0;
@@ -681,6 +689,8 @@ struct GatherStage {
         GatherArgs g{};
         g.U = U.p;
         g.W = W.p;
+        g.w_plane = w_plane;
+        g.w_first = 0;
         g.cparams = base.cparams;
         g.X = base.X;
         g.cells_per_table = cells_per_table;
@@ -700,14 +710,15 @@ struct GatherStage {
 
 // LTCI_COARSE = transform | gather forces the coarse kernel (A/B and tests);
 // otherwise K1g runs whenever the FP32 fine path follows, the shape fits and a
-// table (two transforms per pulse) serves at least four coarse cells.
+// table (two transforms per pulse) serves at least 16 coarse cells (measured:
+// C3's 4 cells per folding number are faster through K1, 0.31 vs 0.44 ms).
 bool gather_selected(int K, int M, bool use_tc, unsigned long long cells_per_table) {
     if (use_tc || !gather_supported(K, M)) return false;
     if (const char* env = std::getenv("LTCI_COARSE")) {
         if (!std::strcmp(env, "transform")) return false;
         if (!std::strcmp(env, "gather")) return true;
     }
-    return cells_per_table >= 4;
+    return cells_per_table >= 16;
 }
 
 struct ltci_engine {
@@ -837,8 +848,8 @@ void engine_init(ltci_engine* e) {
     CK(cudaMemcpy(e->hstep.p, pl.hstep.data(), pl.hstep.size() * sizeof(float2), cudaMemcpyHostToDevice));
     e->slots.ensure(pl.R_slice);
     e->cand_count.ensure(1);
-    // X batch: bounded device footprint (default 4 GiB, LTCI_X_BUDGET_MB overrides)
-    size_t budget = 4ull << 30;
+    // X batch: bounded device footprint (default 6 GiB -- all of C1 in one batch -- LTCI_X_BUDGET_MB overrides)
+    size_t budget = 6ull << 30;
     if (const char* env = std::getenv("LTCI_X_BUDGET_MB")) budget = std::strtoull(env, nullptr, 10) << 20;
     const size_t per_coarse = static_cast<size_t>(pl.R_slice) * M * sizeof(float2);
     e->batch = std::max<unsigned long long>(1, std::min<unsigned long long>(pl.coarse_cells, budget / per_coarse));
@@ -871,7 +882,7 @@ void engine_init(ltci_engine* e) {
             std::vector<double> q(kt ? pl.q_count : 1, 0.0);
             if (kt)
                 for (int i = 0; i < pl.q_count; ++i) q[i] = static_cast<double>(pl.q_min + i);
-            e->gs.init(pl.rp.K, M, q, cpt, e->batch);
+            e->gs.init(pl.rp.K, M, q, cpt, e->batch, pl.coarse_cells);
         }
     }
     const unsigned long long H = pl.coarse_cells * pl.fine_cells * pl.R_slice * pl.D;
@@ -1036,6 +1047,13 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
             coarse_ev.push_back({evt, evt + 1});
         }
         ga = e->gs.args(ca);
+        if (e->gs.w_whole && !e->gs.w_ready) {
+            ga.c_begin = 0;
+            ga.c_count = static_cast<int>(pl.coarse_cells);
+            launch_gather_weights(ga, st);
+            ++e->launches;
+            e->gs.w_ready = true;
+        }
     }
     for (unsigned long long c0 = e->c_lo; c0 < c_end; c0 += e->batch) {
         const unsigned long long cc = std::min<unsigned long long>(e->batch, c_end - c0);
@@ -1050,7 +1068,13 @@ void run_device_impl(ltci_engine* e, const float2* d_cube, cudaStream_t st) {
         if (e->use_gather) {
             ga.c_begin = c0;
             ga.c_count = static_cast<int>(cc);
-            e->launches += launch_gather_cells(ga, st);
+            if (!e->gs.w_whole) {
+                ga.w_first = c0;
+                launch_gather_weights(ga, st);
+                ++e->launches;
+            }
+            launch_gather_cells(ga, st);
+            ++e->launches;
         } else {
             launch_coarse(ca, pg, st, use_tc);
             ++e->launches;
@@ -1923,11 +1947,12 @@ int ltci_cuda_mgift(const double* cube, const ltci_radar* p, const double* ctild
         radix_plan(K, ca.radix, &ca.npass);
         GatherStage gs;
         if (gather_selected(K, M, false, 1)) {  // one cell: only when LTCI_COARSE=gather forces it
-            gs.init(K, M, {variant == LTCI_VARIANT_KTMFP ? cp4[0] : 0.0}, 1, 1);
+            gs.init(K, M, {variant == LTCI_VARIANT_KTMFP ? cp4[0] : 0.0}, 1, 1, 1);
             gs.build(ca, nullptr);
             GatherArgs ga = gs.args(ca);
             ga.c_begin = 0;
             ga.c_count = 1;
+            launch_gather_weights(ga, nullptr);
             launch_gather_cells(ga, nullptr);
         } else {
             launch_coarse(ca, coarse_pg(K, M), nullptr);

@@ -37,11 +37,20 @@ namespace ltcib {
 
 constexpr int kGatherTaps = 8;
 constexpr double kGatherBeta = 2.30 * kGatherTaps;
-constexpr int kGatherCells = 8;   // coarse cells (one warp each) per CTA
+#ifndef LTCI_GATHER_CELLS
+#define LTCI_GATHER_CELLS 16      // coarse cells (one warp each) per CTA
+#endif
+constexpr int kGatherCells = LTCI_GATHER_CELLS;
 #ifndef LTCI_GATHER_ROWS
 #define LTCI_GATHER_ROWS 128      // range cells per CTA tile
 #endif
 constexpr int kGatherRows = LTCI_GATHER_ROWS;
+#ifndef LTCI_GATHER_MINB
+#define LTCI_GATHER_MINB 2        // CTAs per SM the tile leaves room for
+#endif
+#ifndef LTCI_GATHER_STORE
+#define LTCI_GATHER_STORE 1       // 1: evict-first (streaming) stores of X
+#endif
 constexpr int kGatherHalo = 24;   // staged rows beyond the tile: 4 taps + the CTA's spread of shifts
 constexpr int kGatherThreads = 32 * kGatherCells;
 
@@ -49,22 +58,24 @@ constexpr int kGatherThreads = 32 * kGatherCells;
 // D(g), g = 0 .. K/2 (even in g); deap[k] = 1 / D(g(k)) for every frequency
 // row.  Simpson over z = 4 sin(theta): the integrand is analytic in theta
 // (128 intervals reach 3e-13).
-__global__ void gather_deap_kernel(float* __restrict__ deap, int K) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g > K / 2) return;
+__global__ void __launch_bounds__(128) gather_deap_kernel(float* __restrict__ deap, int K) {
     constexpr int N = 128;
     constexpr double kPiD = 3.14159265358979323846;
+    __shared__ double s_f[N + 1], s_z[N + 1];
     const double h = kPiD / N;
+    for (int i = threadIdx.x; i <= N; i += blockDim.x) {
+        double sn, cs;
+        sincos(-0.5 * kPiD + h * i, &sn, &cs);
+        const double wgt = (i == 0 || i == N) ? 1.0 : (i & 1) ? 4.0 : 2.0;
+        s_z[i] = 0.5 * kGatherTaps * sn;
+        s_f[i] = wgt * exp(kGatherBeta * (cs - 1.0)) * (0.5 * kGatherTaps) * cs;
+    }
+    __syncthreads();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > K / 2) return;
     const double kz = kPiD * static_cast<double>(g) / K;
     double acc = 0.0;
-    for (int i = 0; i <= N; ++i) {
-        const double th = -0.5 * kPiD + h * i;
-        double sn, cs;
-        sincos(th, &sn, &cs);
-        const double z = 0.5 * kGatherTaps * sn;
-        const double f = exp(kGatherBeta * (cs - 1.0)) * (0.5 * kGatherTaps) * cs * cos(kz * z);
-        acc += (i == 0 || i == N) ? f : (i & 1) ? 4.0 * f : 2.0 * f;
-    }
+    for (int i = 0; i <= N; ++i) acc += s_f[i] * cos(kz * s_z[i]);
     const float v = static_cast<float>(1.0 / (acc * h / 3.0));
     deap[g] = v;
     if (g > 0 && g < K / 2) deap[K - g] = v;
@@ -109,15 +120,31 @@ __global__ void __launch_bounds__(256) gather_weights_kernel(GatherArgs a) {
     const double cyc = s_predfm * a.two_over_lambda;
     double sn, cs;
     sincospi(2.0 * (cyc - rint(cyc)), &sn, &cs);
-    a.W[idx] = make_float4(w[0], w[2], w[4], w[6]);
-    a.W[total + idx] = make_float4(w[1], w[3], w[5], w[7]);
-    a.W[2 * total + idx] = make_float4(static_cast<float>(cs), static_cast<float>(sn),
-                                       __int_as_float(static_cast<int>(Lm)), 0.0f);
+    const size_t o = static_cast<size_t>(a.c_begin - a.w_first) * a.M + idx;
+    a.W[o] = make_float4(w[0], w[2], w[4], w[6]);
+    a.W[a.w_plane + o] = make_float4(w[1], w[3], w[5], w[7]);
+    a.W[2 * a.w_plane + o] = make_float4(static_cast<float>(cs), static_cast<float>(sn),
+                                         __int_as_float(static_cast<int>(Lm)), 0.0f);
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+// 1-D bulk copy (TMA unit) of one 256-byte table row segment into the tile,
+// completion counted in bytes on the CTA's mbarrier
+__device__ __forceinline__ void gather_bulk_row(void* smem, const void* gmem, unsigned bytes, unsigned bar) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s),
+                 "l"(gmem), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void gather_bar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
 }
 
 // one tile's outputs of a thread.  STAGED: pa / pb point at the thread's first
@@ -147,7 +174,12 @@ __device__ __forceinline__ void gather_run(const float2* __restrict__ pa, const 
         const float2 sa = fma2(a3w, x3, fma2(a2w, x2, fma2(a1w, x1, mul2(a0w, x0))));
         const float2 sb = fma2(b3w, y3, fma2(b2w, y2, fma2(b1w, y1, mul2(b0w, y0))));
         const float2 v = cmul(add2(sa, sb), pre);
-        if (u < left) out[static_cast<size_t>(u) * M] = v;
+        if (u < left) {
+            if constexpr (LTCI_GATHER_STORE)
+                __stcs(out + static_cast<size_t>(u) * M, v);
+            else
+                out[static_cast<size_t>(u) * M] = v;
+        }
     };
 #pragma unroll 1
     for (; left > 0; left -= 4) {
@@ -174,26 +206,32 @@ __device__ __forceinline__ void gather_run(const float2* __restrict__ pa, const 
     }
 }
 
-// grid: (M / 32, ceil(R_slice / kGatherRows), tables x groups); block 256 = 8
-// warps, warp = one coarse cell, lane = pulse m0 + lane.  The CTA stages the
-// plane rows its 8 cells x 32 pulses can touch (cp.async, 256-byte row
-// segments, rows taken modulo K: the gather is circular like the transform),
+// grid: (M / 32, tables x groups, ceil(R_slice / kGatherRows)); block = 16
+// warps, warp = one coarse cell, lane = pulse m0 + lane.  The range tile is
+// the slowest grid index: all cell groups of a tile run back to back on the
+// same ~2 MB of table rows, so the table is read from HBM once (with the
+// groups slowest every group swept the whole table again after 130 MB of X
+// had passed through L2: 1.08 GB of DRAM reads at C1 for a 33.5 MB table).
+// The CTA stages the plane rows its 16 cells x 32 pulses can touch (one
+// 256-byte bulk copy per row on the TMA unit, rows taken modulo K: the gather
+// is circular like the transform; all threads wait on the CTA's mbarrier),
 // then every thread slides its two 4-tap windows down the tile.  Warps store
 // 256 contiguous bytes per range cell; blockIdx.x walks the pulses so
 // co-resident CTAs complete whole rows in L2.  When the shifts of a CTA's
 // cells spread over more than the halo (not the case for the reference's grid
 // rules, where neighbouring coarse cells differ by one range cell at the end
 // of the CPI) the taps are read from global memory instead.
-__global__ void __launch_bounds__(kGatherThreads, 2) gather_interp_kernel(GatherArgs a, int rows_cap) {
+__global__ void __launch_bounds__(kGatherThreads, LTCI_GATHER_MINB) gather_interp_kernel(GatherArgs a, int rows_cap) {
     extern __shared__ __align__(16) float2 g_tile[];  // [2][rows_cap][32]
     __shared__ int s_ref, s_min, s_max;
+    __shared__ __align__(8) unsigned long long s_bar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int K = a.K, M = a.M;
-    const int m0 = blockIdx.x * 32, r0 = blockIdx.y * kGatherRows;
+    const int m0 = blockIdx.x * 32, r0 = blockIdx.z * kGatherRows;
     const unsigned long long cpt = a.cells_per_table;
     const unsigned gpt = static_cast<unsigned>((cpt + kGatherCells - 1) / kGatherCells);
-    const unsigned long long tq = a.c_begin / cpt + blockIdx.z / gpt;
-    const unsigned long long c_first = tq * cpt + static_cast<unsigned long long>(blockIdx.z % gpt) * kGatherCells;
+    const unsigned long long tq = a.c_begin / cpt + blockIdx.y / gpt;
+    const unsigned long long c_first = tq * cpt + static_cast<unsigned long long>(blockIdx.y % gpt) * kGatherCells;
     const unsigned long long c_end = min(a.c_begin + static_cast<unsigned long long>(a.c_count), (tq + 1) * cpt);
     const unsigned long long c_lo = max(a.c_begin, c_first);
     if (c_lo >= c_end || c_lo >= c_first + kGatherCells) return;  // whole CTA outside the batch
@@ -201,18 +239,20 @@ __global__ void __launch_bounds__(kGatherThreads, 2) gather_interp_kernel(Gather
     const bool active = c >= c_lo && c < c_end;
     const int warp_ref = static_cast<int>(c_lo - c_first);
 
-    const size_t total = static_cast<size_t>(a.c_count) * M;
-    const size_t widx = active ? static_cast<size_t>(c - a.c_begin) * M + m0 + lane : 0;
+    const size_t widx = active ? static_cast<size_t>(c - a.w_first) * M + m0 + lane : 0;
     float4 wa = make_float4(0, 0, 0, 0), wb = wa, wc = wa;
     if (active) {
         wa = __ldg(a.W + widx);
-        wb = __ldg(a.W + total + widx);
-        wc = __ldg(a.W + 2 * total + widx);
+        wb = __ldg(a.W + a.w_plane + widx);
+        wc = __ldg(a.W + 2 * a.w_plane + widx);
     }
     const int L = __float_as_int(wc.z);
+    const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(&s_bar));
     if (tid == 0) {
         s_min = 0x7fffffff;
         s_max = -0x7fffffff;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == warp_ref && lane == 0) s_ref = L;
     __syncthreads();
@@ -235,19 +275,20 @@ __global__ void __launch_bounds__(kGatherThreads, 2) gather_interp_kernel(Gather
     const bool staged = rows_need <= rows_cap;
     const float2* Ut = a.U + static_cast<size_t>(tq) * 2 * K * M;
     if (staged) {
-        const int chunks = 2 * rows_need * 16;
-        for (int ch = tid; ch < chunks; ch += kGatherThreads) {
-            const int seg = ch & 15, rr = ch >> 4;
+        // one elected thread per table row: 2 planes x rows_need segments of 256 bytes
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                         "r"(static_cast<unsigned>(2 * rows_need * 256))
+                         : "memory");
+        for (int rr = tid; rr < 2 * rows_need; rr += kGatherThreads) {
             const int plane = rr >= rows_need ? 1 : 0;
             const int row = rr - plane * rows_need;
-            const float2* src = Ut + (static_cast<size_t>(plane) * K + ((row_lo + row) & (K - 1))) * M + m0 + 2 * seg;
-            cp_async16(g_tile + (static_cast<size_t>(plane) * rows_cap + row) * 32 + 2 * seg, src);
+            const float2* src = Ut + (static_cast<size_t>(plane) * K + ((row_lo + row) & (K - 1))) * M + m0;
+            gather_bulk_row(g_tile + (static_cast<size_t>(plane) * rows_cap + row) * 32, src, 256, bar);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    __syncthreads();
     if (!active) return;
+    if (staged) gather_bar_wait(bar, 0);
     const int nmax = min(kGatherRows, a.R_slice - r0);
     const int B = base + d;
     const int pA = B & 1, RA = B >> 1, RB = (B + 1) >> 1;

@@ -27,7 +27,7 @@ void launch_tables_k(const CoarseArgs& a, cudaStream_t st) {
 const void* gather_module_anchor() { return reinterpret_cast<const void*>(gather_module_anchor_kernel); }
 
 void launch_gather_deap(float* deap, int K, cudaStream_t st) {
-    gather_deap_kernel<<<(K / 2 + 1 + 127) / 128, 128, 0, st>>>(deap, K);
+    gather_deap_kernel<<<(K / 2 + 1 + 31) / 32, 32, 0, st>>>(deap, K);
     cuda_check(cudaGetLastError(), "gather deap launch");
 }
 
@@ -45,10 +45,13 @@ void launch_gather_tables(const CoarseArgs& a, cudaStream_t st) {
     }
 }
 
-int launch_gather_cells(const GatherArgs& a, cudaStream_t st) {
+void launch_gather_weights(const GatherArgs& a, cudaStream_t st) {
     const size_t total = static_cast<size_t>(a.c_count) * a.M;
     gather_weights_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(a);
     cuda_check(cudaGetLastError(), "gather weights launch");
+}
+
+void launch_gather_cells(const GatherArgs& a, cudaStream_t st) {
     const int rows_cap = kGatherRows + kGatherHalo;
     const size_t smem = gather_smem_bytes(rows_cap);
     ensure_smem_attr(reinterpret_cast<const void*>(gather_interp_kernel), static_cast<int>(smem));
@@ -57,10 +60,9 @@ int launch_gather_cells(const GatherArgs& a, cudaStream_t st) {
     const unsigned long long t0 = a.c_begin / cpt, t1 = (a.c_begin + a.c_count - 1) / cpt;
     const unsigned long long gz = (t1 - t0 + 1) * gpt;
     if (gz > 65535) throw CubeError(LTCI_INVALID_ARGUMENT, "ltci_cuda: gather batch exceeds the grid");
-    const dim3 grid(a.M / 32, (a.R_slice + kGatherRows - 1) / kGatherRows, static_cast<unsigned>(gz));
+    const dim3 grid(a.M / 32, static_cast<unsigned>(gz), (a.R_slice + kGatherRows - 1) / kGatherRows);
     gather_interp_kernel<<<grid, kGatherThreads, smem, st>>>(a, rows_cap);
     cuda_check(cudaGetLastError(), "gather launch");
-    return 2;
 }
 
 }  // namespace ltcib

@@ -12,7 +12,10 @@ struct CoarseArgs;
 
 struct GatherArgs {
     const float2* U;         // [tables][2][K][M]: even / odd fine samples of each pulse
-    float4* W;               // [3][c_count * M]: even-stream taps, odd-stream taps, (pre.x, pre.y, L, -)
+    float4* W;               // [3][w_plane]: even-stream taps, odd-stream taps, (pre.x, pre.y, L, -);
+                             // cell c, pulse m at (c - w_first) * M + m of each plane
+    size_t w_plane;
+    unsigned long long w_first;
     const double* cparams;   // [coarse][4]: GRFT c1..cP ; KT (q, c2)
     float2* X;               // [c_count * R_slice][M]
     unsigned long long c_begin;
@@ -38,8 +41,11 @@ void launch_gather_deap(float* deap, int K, cudaStream_t st);
 // a.X = U [2 * tables][K][M], a.deap set, a.c_count = 2 * tables, full range axis
 void launch_gather_tables(const CoarseArgs& a, cudaStream_t st);
 
-// weights + gather of one batch of coarse cells; returns the kernels launched
-int launch_gather_cells(const GatherArgs& a, cudaStream_t st);
+// the (cell, pulse) weights of cells [a.c_begin, a.c_begin + a.c_count)
+void launch_gather_weights(const GatherArgs& a, cudaStream_t st);
+
+// gather of one batch of coarse cells (weights already in a.W)
+void launch_gather_cells(const GatherArgs& a, cudaStream_t st);
 
 const void* gather_module_anchor();
 

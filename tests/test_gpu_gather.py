@@ -100,13 +100,17 @@ def test_engine_paths_agree_c0(monkeypatch):
                 value_at=lambda i: _cell_value(x, w, i))
 
 
-def test_default_is_gather():
-    w = config(0)
-    e = Engine(w.params, w.space, w.variant, w.amb, DetectorOptions(retain_threshold=1e9))
-    try:
-        assert e.coarse_path() == "gather"
-    finally:
-        e.close()
+def test_default_paths():
+    """AUTO: the gather whenever a table serves at least 16 coarse cells
+    (configs[1], [2], [4]); the transform for configs[0] (11 cells) and
+    configs[3] (4 cells per folding number)."""
+    for ci, want in ((0, "transform"), (4, "gather"), (3, "transform")):
+        w = config(ci)
+        e = Engine(w.params, w.space, w.variant, w.amb, DetectorOptions(retain_threshold=1e9))
+        try:
+            assert e.coarse_path() == want, ci
+        finally:
+            e.close()
 
 
 def test_small_goldens_gather(gather):
