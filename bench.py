@@ -332,6 +332,12 @@ def main():
     w = w_full = configs.config(args.config)
     if args.coarse_slice:
         w = configs.sliced(w, args.coarse_slice, args.coarse_rest)
+        # a coarse-cell slice is a rate sample of the full job: it runs the coarse kernel the full
+        # job's AUTO rule picks (K1g from 16 coarse cells per table; the slice alone may be below
+        # that), and pays the full job's once-per-CPI table build on its few cells (pessimistic)
+        if "LTCI_COARSE" not in os.environ and w_full.variant == 0 and \
+                int(np.prod([g.count for g in w_full.space.coarse])) >= 16:
+            os.environ["LTCI_COARSE"] = "gather"
     if args.impl == "reference":
         run_reference(args, w, ws, rank, w_full)
         return

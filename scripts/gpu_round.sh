@@ -18,9 +18,9 @@ python scripts/bench_io.py > gpurun_out/side_io.log 2>&1
 python scripts/time_calls.py > gpurun_out/side_calls.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv python scripts/profile_step.py --config 1 > gpurun_out/ncu_launch_c1.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python scripts/profile_step.py --config 3 > gpurun_out/ncu_launch_c3.log 2>&1
-for spec in "c1:1:fine_fft_tm|coarse:2" "c3:3:range_fft|keystone_tiled|fine_fft_tm|coarse:4" "c0:0:fine_fft_tm:1" "c4:4:fine_fft_tm:1"; do
+for spec in "c1:1:fine_fft_tm|gather_interp|coarse_rm:3" "c3:3:range_fft|keystone_tiled|fine_fft_tm|coarse:4" "c0:0:fine_fft_tm:1" "c4:4:fine_fft_tm|gather_interp:2"; do
   IFS=: read name cfg regex count <<< "$spec"
-  ncu --set full --import-source on --clock-control none -k regex:"$regex" -c $count -o /tmp/ncu/$name \
+  ncu -f --set full --import-source on --clock-control none -k regex:"$regex" -c $count -o /tmp/ncu/$name \
       python scripts/profile_step.py --config $cfg > gpurun_out/ncu_$name.log 2>&1
   python scripts/ncu_brief.py /tmp/ncu/$name.ncu-rep > gpurun_out/ncu_${name}_brief.txt 2>&1
 done

@@ -43,7 +43,7 @@ def test_mgift_gather_matches_reference_golden(gather):
 
 
 @pytest.mark.parametrize("M,K", [(32, 64), (64, 128), (128, 256), (256, 512), (512, 1024), (1024, 2048),
-                                 (256, 4096), (32, 8192)])
+                                 (256, 4096), (2048, 4096), (32, 8192)])
 def test_mgift_gather_all_sizes(gather, M, K):
     """White noise over the whole band (the worst case for the interpolation
     window), shifts of every size and sign, third order, the keystone variant
@@ -149,3 +149,24 @@ def test_random_spaces_gather_vs_port(gather):
         rk = O.port_ds(x, p, s, opt, variant=1, amb=amb)
         assert np.abs(gk.dense - rk.dense).max() / np.abs(rk.dense).max() <= TOL
         check_peaks(gk.peak_index, gk.peak_value, rk.peak_index, rk.peak_value, value_at=lambda i: rk.dense[i])
+
+
+def test_gather_wide_shift_spread(gather):
+    """Coarse cells 40 range-migration steps apart: the shifts of one CTA's
+    cells spread past the staged halo and the taps come from global memory
+    (the fallback path), with wrap-around at both ends of the range axis."""
+    from paper_2403_06788_b200.configs import baseline_space
+    from paper_2403_06788_b200.model import Grid
+    p = RadarParams.create(3e9, 20e6, 20e6, 1000.0, 64, 256)
+    s = baseline_space(p, [(-2000.0, 2000.0), (-6.0, 6.0)])
+    g0, f1 = s.coarse[0], s.fine[1]
+    assert g0.count >= 32
+    s.coarse[0] = Grid(g0.start * 40.0, g0.step * 40.0, g0.count)
+    s.fine[1] = Grid(f1.start, f1.step * 30.0, 5)
+    x = scene.to_complex64_roundtrip(
+        scene.add_noise(scene.synthesize_cube(p, [(0.3, [100 * p.delta_R(), 0.0, 1.0])]), 1.0 / p.K, 3))
+    opt = DetectorOptions(retain_threshold=0.5, keep_dense=True)
+    gm = ds_grft(x, p, s, opt)
+    rm = O.port_ds(x, p, s, opt)
+    assert np.abs(gm.dense - rm.dense).max() / np.abs(rm.dense).max() <= TOL
+    check_peaks(gm.peak_index, gm.peak_value, rm.peak_index, rm.peak_value, value_at=lambda i: rm.dense[i])
