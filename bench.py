@@ -167,15 +167,32 @@ def n_coarse_cells(w) -> int:
 
 
 # coarse-stage (K1, plus K0/K4 for configs[3]) time relative to the fine stage,
-# measured on one B200: C0 0.065, C1 0.021, C3 0.022 (profiles/r02_bench_c*.json)
-COARSE_OVER_FINE = 0.03
+# coarse / fine stage time on one B200 (profiles/r02_bench_c*.json): the transform kernel K1
+# (C0 0.065, C3 0.022) and the interpolating gather K1g (C1 0.009, C4 0.013)
+COARSE_OVER_FINE = {"transform": 0.03, "gather": 0.01}
+# share of the coarse stage a range-cell shard repeats on every rank: all of it with K1 (the
+# K-point transforms are needed whatever rows are kept), only the per-pulse tables with K1g
+# (22 us of 0.92 ms at C1)
+COARSE_REPEATED = {"transform": 1.0, "gather": 0.03}
+
+
+def coarse_path_of(w) -> str:
+    """The engine's AUTO rule (csrc/engine.cu gather_selected) for the FP32 fine path."""
+    forced = os.environ.get("LTCI_COARSE")
+    if forced in ("transform", "gather"):
+        return forced
+    p = w.params
+    per_table = n_coarse_cells(w) // (w.amb.count() if w.variant == 1 else 1)
+    return "gather" if p.K >= 64 and 256 <= p.M and per_table >= 16 else "transform"
 
 
 def plan_shard(w, ws: int, requested: str) -> str:
     """The job's partition across ``ws`` ranks (the same answer in both arms).
     auto: the partition with the smaller busiest-rank time -- coarse-cell
-    shards pay ceil(C / ws) whole cells on the busiest rank, range-cell shards
-    split the fine stage evenly but repeat the coarse stage on every rank."""
+    shards pay ceil(C / ws) whole cells on the busiest rank; range-cell shards
+    (BASELINE's partition) split the fine stage and the gather evenly and
+    repeat, on every rank, the part of the coarse stage that does not depend
+    on the rows kept."""
     if w.cpis > 1:
         return "cpis"
     if requested != "auto":
@@ -183,8 +200,10 @@ def plan_shard(w, ws: int, requested: str) -> str:
     C, R = n_coarse_cells(w), w.space.roi.count()
     if ws == 1 or C < ws:
         return "coarse" if C >= ws else "rows"
-    coarse_cost = (1.0 + COARSE_OVER_FINE) * (-(-C // ws)) / C
-    rows_cost = (-(-R // ws)) / R + COARSE_OVER_FINE
+    path = coarse_path_of(w)
+    cof, rep = COARSE_OVER_FINE[path], COARSE_REPEATED[path]
+    coarse_cost = (1.0 + cof) * (-(-C // ws)) / C
+    rows_cost = (1.0 + cof * (1.0 - rep)) * (-(-R // ws)) / R + cof * rep
     return "coarse" if coarse_cost <= rows_cost else "rows"
 
 
