@@ -330,18 +330,20 @@ class _CAI:
         self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 2}
 
 
-def _ncu_traffic(config_index, kernel):
-    """DRAM bytes per launch of the fine kernel from the committed ncu --set full captures
-    (C1: ``kernel`` in profiles/r01_ncu_c1.json; other configs: profiles/r01_ncu_traffic.json)."""
-    if config_index != 1:
-        path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
-        if kernel.startswith("fine_tc") or not os.path.exists(path):
-            return None
-        return json.load(open(path)).get(str(config_index), {}).get("traffic_bytes_per_launch")
-    path = os.path.join(ROOT, "profiles", "r01_ncu_c1.json")
-    if not os.path.exists(path):
+def _ncu_traffic(config_index, kernel, stage="fine"):
+    """DRAM bytes per launch of the fine (or coarse) kernel from the committed ncu --set full
+    captures of this round (profiles/r02_ncu_traffic.json, from profiles/r02_ncu_c*.txt)."""
+    path = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
+    if kernel.startswith("fine_tc") or not os.path.exists(path):
+        if kernel.startswith("fine_tc") and config_index == 1:
+            old = os.path.join(ROOT, "profiles", "r01_ncu_c1.json")
+            if os.path.exists(old):
+                return json.load(open(old)).get(kernel, {}).get("traffic_bytes_per_launch")
         return None
-    return json.load(open(path)).get(kernel, {}).get("traffic_bytes_per_launch")
+    ent = json.load(open(path)).get(str(config_index), {})
+    if stage == "coarse":
+        ent = ent.get("coarse", {})
+    return ent.get("traffic_bytes_per_launch")
 
 
 def main():
@@ -662,7 +664,7 @@ def main():
                     "traffic": _ncu_traffic(args.config, "fine_fft_tm_kernel<0>")
                     if 256 <= p.M <= 2048 and (args.config != 2 or (args.coarse_slice == 1 and args.coarse_rest == 1))
                     else None,
-                    "traffic_source": ("profiles/r01_ncu_c1.json" if args.config == 1 else "profiles/r01_ncu_traffic.json")
+                    "traffic_source": "profiles/r02_ncu_traffic.json"
                     + " (ncu --set full, DRAM bytes per launch)",
                     "peak_source": "measured in-run FFMA chain microbenchmark (ltci_cuda_measure_fp32_peak)",
                     "algorithmic": "per (row, fine cell): 6M chirp + 5M log2M FFT + 3D |Y|^2 flop",
@@ -676,6 +678,8 @@ def main():
                                       if st["coarse_ms"] > 0 else None,
                                       "fp32_algorithmic": "per (coarse cell, pulse): 5 K log2 K FFT + 8 K ramp",
                                       "path": eng.coarse_path(),
+                                      "traffic": _ncu_traffic(args.config, "coarse", stage="coarse")
+                                      if not args.coarse_slice and ws == 1 else None,
                                       "note": ("K1g (gather.cuh): 8-tap interpolation of 2x-oversampled range "
                                                "profiles tabulated once per pulse (type-2 NUFFT, 1.3e-7 of the "
                                                "profile maximum); table build + weights + gather are all inside "
