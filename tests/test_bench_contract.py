@@ -57,3 +57,31 @@ def test_reference_arm_line_matches_b200_arm_contract():
     cb = line["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["unit"] == unit and cb["value"] == line["value"]
     assert line["e2e"] == {"value": line["value"], "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_bench_coarse_path_and_partition_model():
+    """bench.py mirrors the engine's AUTO rule for the coarse stage (csrc/engine.cu
+    gather_selected) when it plans the N-rank partition: K1g for configs[1], [2], [4];
+    K1 for configs[0] (11 cells) and configs[3] (4 cells per folding number); with K1g
+    a range-cell shard repeats only the per-pulse tables, so C1 takes BASELINE's
+    range-cell partition at N = 8."""
+    import importlib
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    bench = importlib.import_module("bench")
+    from paper_2403_06788_b200 import configs
+    old = os.environ.pop("LTCI_COARSE", None)
+    try:
+        want = {0: "transform", 1: "gather", 2: "gather", 3: "transform", 4: "gather"}
+        for ci, path in want.items():
+            assert bench.coarse_path_of(configs.config(ci)) == path, ci
+        assert bench.plan_shard(configs.config(1), 8, "auto") == "rows"
+        assert bench.plan_shard(configs.config(1), 2, "auto") == "coarse"
+        assert bench.plan_shard(configs.config(0), 8, "auto") == "rows"
+        assert bench.plan_shard(configs.config(4), 8, "auto") == "cpis"
+        assert bench.plan_shard(configs.config(3), 8, "rows") == "rows"
+    finally:
+        if old is not None:
+            os.environ["LTCI_COARSE"] = old
