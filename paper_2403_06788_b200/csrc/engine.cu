@@ -649,7 +649,9 @@ struct GatherStage {
         tables = static_cast<int>(q.size());
         cells_per_table = cpt;
         U.ensure(static_cast<size_t>(tables) * 2 * K * M);
-        w_whole = gather_weight_bytes(plan_cells, M) <= (1ull << 30);
+        size_t cache_cap = 1ull << 30;  // LTCI_GATHER_WCACHE_MB overrides (0: weights per batch)
+        if (const char* env = std::getenv("LTCI_GATHER_WCACHE_MB")) cache_cap = std::strtoull(env, nullptr, 10) << 20;
+        w_whole = gather_weight_bytes(plan_cells, M) <= cache_cap;
         w_ready = false;
         w_plane = static_cast<size_t>(w_whole ? plan_cells : batch) * M;
         W.ensure(3 * w_plane);

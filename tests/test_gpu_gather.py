@@ -197,3 +197,20 @@ def test_engine_paths_agree_full_size(monkeypatch, cfg):
     assert diff.size <= max(3, mt.peak_index.size // 200), diff.size
     check_candidates(mg.cand_index, mg.cand_value, mt.cand_index, mt.cand_value, gamma)
     assert mg.argmax == mt.argmax
+
+
+def test_gather_batched_weights_bit_identical(monkeypatch):
+    """Plans too large for the plan-wide weight cache compute the weights per X
+    batch: with a 24 MiB X budget (several batches at configs[4]'s shape) and
+    the cache disabled the map is bit-identical to the cached single-batch run."""
+    w = config(4)
+    x = scene.to_complex64_roundtrip(w.cube())
+    gamma = detection_threshold(w.params, w.sigma2, 1e-6)
+    monkeypatch.setenv("LTCI_COARSE", "gather")
+    _, ref = _run(w, x, gamma)
+    monkeypatch.setenv("LTCI_X_BUDGET_MB", "24")
+    monkeypatch.setenv("LTCI_GATHER_WCACHE_MB", "0")
+    _, got = _run(w, x, gamma)
+    assert np.array_equal(got.peak_index, ref.peak_index)
+    assert np.array_equal(got.peak_value, ref.peak_value)
+    assert np.array_equal(got.cand_index, ref.cand_index) and np.array_equal(got.cand_value, ref.cand_value)
