@@ -349,6 +349,12 @@ def _ncu_traffic(config_index, kernel, stage="fine"):
 def main():
     args = parse()
     ws, rank, local = dist_env()
+    if ws > 1 or os.environ.get("LTCI_BENCH_FORCE_DIST") == "1":
+        # communicator lines (nRanks, transport) stay on stderr as the run's evidence: INFO is a
+        # superset of the VERSION level the GPU boxes preset (which prints the version line only)
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     from paper_2403_06788_b200 import configs
     w = w_full = configs.config(args.config)
     if args.coarse_slice:
@@ -373,16 +379,17 @@ def main():
     # LTCI_BENCH_SHARED_GPU=1: functional check of the N-rank path on a 1-GPU box
     # (every rank on cuda:0, gloo over host copies); its timings mean nothing
     shared_gpu = ws > 1 and os.environ.get("LTCI_BENCH_SHARED_GPU") == "1"
+    # LTCI_BENCH_FORCE_DIST=1 (under torchrun): run the N-rank code path -- NCCL communicator,
+    # barriers, peak-map gather and device merge, max-over-ranks reduction -- whatever the world
+    # size, so a 1-GPU box executes it over real NCCL with a world of one rank
+    multi = ws > 1 or (os.environ.get("LTCI_BENCH_FORCE_DIST") == "1" and "RANK" in os.environ)
     if shared_gpu:
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    if ws > 1:
+    if multi:
         if shared_gpu:
             dist.init_process_group("gloo")
         else:
-            # communicator lines (nRanks, transport) stay on stderr as the run's evidence
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2403_06788_b200.parallel import PeakGather, RankComm
@@ -450,7 +457,7 @@ def main():
     per_cpi_peaks = torch.empty((len(my_cpis), n_rows, 4), dtype=torch.int32, device=dev)
     lib = _lib.load()
     gather = None
-    if ws > 1 and cpis == 1:
+    if multi and cpis == 1:
         def merge_on_device(gathered, merged):
             _lib.raise_for(lib.ltci_cuda_merge_peaks(ctypes.c_void_p(gathered.data_ptr()), ws, R,
                                                      ctypes.c_void_p(merged.data_ptr()), ctypes.c_void_p(sptr)),
@@ -497,7 +504,7 @@ def main():
     log("timed steps")
     # ---- value: device-timed, L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if ws > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize(dev)
     wall0 = time.perf_counter()
@@ -518,11 +525,11 @@ def main():
             step_local()
             torch.cuda.synchronize(dev)
             extra_steps += 1
-    if ws > 1:
+    if multi:
         dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
+    if multi:
         comm.all_reduce_max(t)
     ms_max = float(t.item())
     total_integ = w.integrations() * cpis  # all ranks together cover every hypothesis of every CPI once
@@ -536,7 +543,7 @@ def main():
     run_dev(eng, d_cubes[0].data_ptr(), sptr)
     st = eng.stats()
     eng.set_timing(False)
-    launches = st["launches"] * len(my_cpis) + (1 if ws > 1 and shard == "coarse" else 0)  # + peak merge
+    launches = st["launches"] * len(my_cpis) + (1 if multi and shard == "coarse" and cpis == 1 else 0)  # + peak merge
 
     log("e2e")
     # ---- e2e: public API from pinned host memory, results back to host
@@ -547,7 +554,7 @@ def main():
     res_bytes = lambda m: 8 + 16 * n_rows + 24 * int(m.cand_index.size)  # noqa: E731
     e2e_lanes = n_lanes
     e2e_steps = args.steps
-    if ws == 1:
+    if not multi:
         # one process streams the job's CPIs step after step through the public API; the
         # lanes keep two in flight (CPI i+1 uploads and runs while CPI i's result drains),
         # so the timed region holds every step's H2D, run and D2H, overlapped as a
@@ -606,7 +613,7 @@ def main():
             if i >= args.warmup:
                 e2e_ms.append((t1 - t0) * 1e3)
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
-    if ws > 1:
+    if multi:
         comm.all_reduce_max(e2e_t)
     e2e_value = total_integ * args.steps / (float(e2e_t.item()) * 1e-3) / 1e9
 
@@ -735,9 +742,9 @@ def main():
             "roofline": roof,
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": int(cube.size * 16 * len(cubes)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": float(e2e_t.item()) / args.steps,
-                    "lanes": e2e_lanes, "steps": e2e_steps if ws == 1 else args.steps,
+                    "lanes": e2e_lanes, "steps": e2e_steps if not multi else args.steps,
                     "pipeline": "public API (Engine.run_host_ptr from pinned f64 + result()), CPIs streamed over "
-                                f"{e2e_lanes} engine lanes" if ws == 1 else "per step: upload, run, result, gather"},
+                                f"{e2e_lanes} engine lanes" if not multi else "per step: upload, run, result, gather"},
             "gpu_launches": int(launches) * args.steps,
             "clocks": dict(clk.summary(), **({"untimed_repeat_steps_sampled": extra_steps} if extra_steps else {})),
             "wall_s_timed_region": wall,
@@ -751,15 +758,17 @@ def main():
             line["cpu_baseline"] = cb
         if shared_gpu:
             line["shared_gpu_functional_check"] = True  # N ranks on one GPU: timings are not a measurement
+        if multi and ws == 1:
+            line["n_rank_path_forced"] = "LTCI_BENCH_FORCE_DIST=1: the N-rank path (NCCL) with a world of one rank"
         dump = os.environ.get("LTCI_BENCH_DUMP_PEAKS")
         if dump and cpis == 1:
             # the job's per-row peak map (R x {idx lo, idx hi, re, im}) after the rank
             # merge of the last e2e step (collectives already done on every rank)
             torch.cuda.synchronize(dev)
-            full = peaks.view(torch.int32) if ws == 1 else gather.full_map()
+            full = peaks.view(torch.int32) if not multi else gather.full_map()
             np.save(dump, full.cpu().numpy())
         print(json.dumps(line))
-    if ws > 1:
+    if multi:
         dist.destroy_process_group()
     for e in lane_engs:
         e.close()
