@@ -89,6 +89,12 @@ struct FreqPulseCube {
     std::vector<cplx> data;  // sample (k, m) at data[k + K*m]
 };
 
+// range-pulse cube (proj/include/ltci/cube.hpp:30-47): sample (n, m) at data[n + K*m]
+struct RangePulseCube {
+    RadarParams params;
+    std::vector<cplx> data;
+};
+
 enum class TrajectoryPolicy { ZeroOutside, Wrap, Error };
 
 struct DetectorOptions {
@@ -131,6 +137,11 @@ struct DetectionMap {
 
 // proj/include/ltci/detectors.hpp:25-26
 DetectionMap fd_grft(const FreqPulseCube& cube, const SingleScaleSpace& space, const DetectorOptions& opt = {});
+// proj/include/ltci/detectors.hpp:29-31 (std::out_of_range under TrajectoryPolicy::Error)
+DetectionMap td_grft(const RangePulseCube& cube, const SingleScaleSpace& space, const DetectorOptions& opt = {});
+// proj/include/ltci/detectors.hpp:33-37
+DetectionMap kt_mfp(const FreqPulseCube& cube, const AmbiguitySpace& amb, const SingleScaleSpace& space,
+                    const DetectorOptions& opt = {});
 DetectionMap ds_grft(const FreqPulseCube& cube, const DualScaleSpace& space, const DetectorOptions& opt = {});
 DetectionMap ds_kt_mfp(const FreqPulseCube& cube, const AmbiguitySpace& amb, const DualScaleSpace& space,
                        const DetectorOptions& opt = {});

@@ -15,6 +15,8 @@
  *                                               proj/src/detectors.cpp:451-481
  *   ltci_cuda_keystone     -> ltci::keystone   proj/include/ltci/transforms.hpp:40
  *   ltci_cuda_mgift        -> ltci::mgift      proj/include/ltci/transforms.hpp:52-53
+ *   ltci_cuda_td_grft      -> ltci::td_grft    proj/include/ltci/detectors.hpp:29-31
+ *   ltci_cuda_kt_mfp       -> ltci::kt_mfp     proj/include/ltci/detectors.hpp:33-37
  *   ltci_cuda_gft          -> ltci::gft        proj/include/ltci/transforms.hpp:74-75
  *   ltci_cuda_detection_threshold -> ltci::detection_threshold
  *                                               proj/include/ltci/detectors.hpp:55
@@ -53,7 +55,8 @@ enum {
     LTCI_RUNTIME_ERROR = 3,    /* std::runtime_error (CUDA failure) */
     LTCI_BAD_ALLOC = 4,        /* std::bad_alloc (result too large) */
     LTCI_NO_DEVICE = 5,        /* no CUDA device / extension missing */
-    LTCI_IO_ERROR = 6          /* ltci::IoError (cube file container) */
+    LTCI_IO_ERROR = 6,         /* ltci::IoError (cube file container) */
+    LTCI_OUT_OF_RANGE = 7      /* std::out_of_range (td_grft, TrajectoryPolicy::Error) */
 };
 
 /* detector kinds, same order as ltci::DetectorKind (detection.hpp:12) */
@@ -182,6 +185,24 @@ void ltci_cuda_free_map(ltci_detection_map *map);
  * index).  Extension: an ROI outside [0, K) is LTCI_INVALID_ARGUMENT. */
 int ltci_cuda_fd_grft(const double *cube, const ltci_radar *cube_params, const ltci_single_space *space,
                       const ltci_options *opt, ltci_detection_map **out);
+/* ltci::td_grft (proj/include/ltci/detectors.hpp:29-31, proj/src/detectors.cpp:199-264):
+ * the single-scale time-domain GRFT over a RANGE-pulse cube (data[n + K*m]):
+ * per motion cell and ROI row the sum over pulses of the nearest-bin sample
+ * along the trajectory, n(m) = lround(n0 + (2 fs / c) S(t_m)), times
+ * exp(j 4 pi S(t_m) / lambda).  opt->trajectory is the reference's
+ * TrajectoryPolicy for bins outside [0, K): 0 contribute zero, 1 wrap modulo
+ * K, 2 raise (LTCI_OUT_OF_RANGE = std::out_of_range, same message).  Map
+ * contract as fd_grft's (kind LTCI_TD_GRFT; counter mf += 1 per (cell, row)). */
+int ltci_cuda_td_grft(const double *range_cube, const ltci_radar *cube_params, const ltci_single_space *space,
+                      const ltci_options *opt, ltci_detection_map **out);
+/* ltci::kt_mfp (proj/include/ltci/detectors.hpp:33-37, proj/src/detectors.cpp:266-326):
+ * keystone once, then per (folding number q, acceleration c2) cell the
+ * matched filter over the full Doppler axis.  `space` must have order 2 (its
+ * velocity grid is unused).  Axes [Folding, Higher 2, Range, Doppler], flat
+ * index ((iq * n2 + i2) * R + r) * M + j, counters kt = 1, mf += K, ifft += M,
+ * fft += R per cell.  Runs the dual-scale keystone cascade with one fine cell. */
+int ltci_cuda_kt_mfp(const double *cube, const ltci_radar *cube_params, const ltci_ambiguity *amb,
+                     const ltci_single_space *space, const ltci_options *opt, ltci_detection_map **out);
 int ltci_cuda_keystone(const double *cube, const ltci_radar *p, int taps, double *out);
 /* keystone on device complex64 cubes (K*M float2, column-major), asynchronous
  * on the given cudaStream_t: the K4 kernel ds_kt_mfp runs, for timing it over

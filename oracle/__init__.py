@@ -59,6 +59,9 @@ def port():
         lib.oracle_gft.argtypes = [C.c_void_p, P(A.CRadar), P(C.c_double), C.c_int, C.c_int, C.c_int, C.c_void_p]
         lib.oracle_keystone.argtypes = [C.c_void_p, P(A.CRadar), C.c_int, C.c_void_p]
         lib.oracle_range_fft.argtypes = [C.c_void_p, P(A.CRadar), C.c_void_p]
+        lib.oracle_td_grft.argtypes = [C.c_void_p, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
+        lib.oracle_kt_mfp.argtypes = [C.c_void_p, P(A.CRadar), P(A.CAmbiguity), P(A.CSingleSpace), P(A.COptions),
+                                      P(A.PMap)]
         _port = lib
     return _port
 
@@ -102,6 +105,8 @@ def ref():
         lib.ref_build_single_scale.argtypes = [P(A.CRadar), C.c_int, P(C.c_double), P(C.c_double), P(C.c_double),
                                                C.c_int, C.c_int, P(A.CSingleSpace)]
         lib.ref_fd_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
+        lib.ref_td_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
+        lib.ref_kt_mfp.argtypes = [vp, P(A.CRadar), P(A.CAmbiguity), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
         lib.ref_extract_single.argtypes = [P(A.CDetectionMap), P(A.CSingleSpace), C.c_double, C.c_int, vp,
                                            P(C.c_int)]
         lib.ref_read_cube_file.argtypes = [C.c_char_p, P(A.CCubeHeader), vp, C.c_uint64]
@@ -362,6 +367,50 @@ def ref_fd(cube, params, space: SingleScaleSpace, opt: Optional[DetectorOptions]
     m = _map(lib, pm, params, lib.ref_free_map)
     m.single = space
     return m
+
+
+def _single_call(fn, lib, free, cube, params, space, opt, amb=None) -> DetectionMap:
+    opt = opt or DetectorOptions()
+    data = _c128(cube)
+    r, s, o = params.to_c(), space.to_c(), opt.to_c()
+    pm = A.PMap()
+    if amb is None:
+        rc = fn(_vp(data), C.byref(r), C.byref(s), C.byref(o), C.byref(pm))
+    else:
+        a = amb.to_c()
+        rc = fn(_vp(data), C.byref(r), C.byref(a), C.byref(s), C.byref(o), C.byref(pm))
+    if rc == 7:  # LTCI_OUT_OF_RANGE: td_grft under TrajectoryPolicy::Error
+        raise IndexError("td_grft: trajectory leaves the cube")
+    _check(rc, lib)
+    m = _map(lib, pm, params, free)
+    m.single, m.amb = space, amb
+    return m
+
+
+def ref_td(range_cube, params, space: SingleScaleSpace, opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    """The reference's td_grft (proj/src/detectors.cpp:199-264) on a range-pulse cube."""
+    lib = ref()
+    return _single_call(lib.ref_td_grft, lib, lib.ref_free_map, range_cube, params, space, opt)
+
+
+def ref_kt(cube, params, amb: AmbiguitySpace, space: SingleScaleSpace,
+           opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    """The reference's kt_mfp (proj/src/detectors.cpp:266-326)."""
+    lib = ref()
+    return _single_call(lib.ref_kt_mfp, lib, lib.ref_free_map, cube, params, space, opt, amb)
+
+
+def port_td(range_cube, params, space: SingleScaleSpace, opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    """Our C restatement of td_grft (oracle/ds_oracle.c oracle_td_grft)."""
+    lib = port()
+    return _single_call(lib.oracle_td_grft, lib, lib.oracle_free_map, range_cube, params, space, opt)
+
+
+def port_kt(cube, params, amb: AmbiguitySpace, space: SingleScaleSpace,
+            opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    """Our C restatement of kt_mfp (oracle/ds_oracle.c oracle_kt_mfp)."""
+    lib = port()
+    return _single_call(lib.oracle_kt_mfp, lib, lib.oracle_free_map, cube, params, space, opt, amb)
 
 
 def ref_extract_single(m: DetectionMap, gamma: float, max_out: int = 4096) -> np.ndarray:

@@ -16,6 +16,8 @@
  *                                                   proj/src/signal_model.cpp:97-107, proj/src/fft.cpp:30-51
  *   oracle_ds          ds_grft / ds_kt_mfp -> run_dual_scale + UnitScan + merge_units
  *                                                   proj/src/detectors.cpp:16-50,337-481
+ *   oracle_td_grft     td_grft (rounded-trajectory sums)   proj/src/detectors.cpp:199-264
+ *   oracle_kt_mfp      kt_mfp (keystone, gift(KtRm), gft)  proj/src/detectors.cpp:266-326
  */
 #include <complex.h>
 #include <math.h>
@@ -528,5 +530,208 @@ int oracle_range_fft(const double *cube_d, const ltci_radar *p, double *out) {
     }
     free(tw);
     free(x);
+    return LTCI_OK;
+}
+
+/* ------------------------------------------- single-scale td_grft / kt_mfp --- */
+/* One scan over cells in index order: UnitScan::consider + merge_units
+ * (proj/src/detectors.cpp:16-50) collapse to this when units are visited in order. */
+typedef struct {
+    double retain;
+    int keep_dense;
+    cand_t *cand;
+    uint64_t ncand, cap;
+    double best_m;
+    uint64_t best_i;
+    cplx best_v;
+    cplx *dense;
+} scan_t;
+
+static void scan_consider(scan_t *sc, uint64_t idx, cplx v) {
+    double m = cabs(v);
+    if (m > sc->retain) {
+        if (sc->ncand == sc->cap) {
+            sc->cap = sc->cap ? 2 * sc->cap : 256;
+            sc->cand = realloc(sc->cand, sizeof(cand_t) * sc->cap);
+        }
+        sc->cand[sc->ncand++] = (cand_t){idx, v};
+    }
+    if (m > sc->best_m || (m == sc->best_m && idx < sc->best_i)) {
+        sc->best_m = m;
+        sc->best_i = idx;
+        sc->best_v = v;
+    }
+    if (sc->keep_dense) sc->dense[idx] = v;
+}
+
+static void scan_finish(scan_t *sc, ltci_detection_map *mp, uint64_t cells) {
+    qsort(sc->cand, sc->ncand, sizeof(cand_t), cmp_cand);
+    mp->n_candidates = sc->ncand;
+    mp->cand_index = malloc(sizeof(uint64_t) * (sc->ncand ? sc->ncand : 1));
+    mp->cand_value = malloc(sizeof(double) * 2 * (sc->ncand ? sc->ncand : 1));
+    for (uint64_t i = 0; i < sc->ncand; ++i) {
+        mp->cand_index[i] = sc->cand[i].idx;
+        mp->cand_value[2 * i] = creal(sc->cand[i].v);
+        mp->cand_value[2 * i + 1] = cimag(sc->cand[i].v);
+    }
+    mp->argmax = sc->best_i;
+    mp->argmax_value[0] = creal(sc->best_v);
+    mp->argmax_value[1] = cimag(sc->best_v);
+    mp->retain_threshold = sc->retain;
+    if (sc->keep_dense) {
+        mp->dense_stored = 1;
+        mp->dense_count = cells;
+        mp->dense = malloc(sizeof(double) * 2 * (cells ? cells : 1));
+        for (uint64_t i = 0; i < cells; ++i) {
+            mp->dense[2 * i] = creal(sc->dense[i]);
+            mp->dense[2 * i + 1] = cimag(sc->dense[i]);
+        }
+    }
+    free(sc->cand);
+    free(sc->dense);
+}
+
+static int same_radar(const ltci_radar *a, const ltci_radar *b) {
+    return a->K == b->K && a->M == b->M && a->fc == b->fc && a->fs == b->fs && a->PRF == b->PRF;
+}
+
+/* td_grft (proj/src/detectors.cpp:199-264) on a range-pulse cube [n + K*m].
+ * opt->trajectory: 0 ZeroOutside, 1 Wrap, 2 Error (returns LTCI_OUT_OF_RANGE). */
+int oracle_td_grft(const double *cube_d, const ltci_radar *p, const ltci_single_space *s, const ltci_options *opt,
+                   ltci_detection_map **out) {
+    const int K = p->K, M = p->M, P = s->order;
+    if (!same_radar(p, &s->radar)) return LTCI_INVALID_ARGUMENT;
+    const int R = s->roi_last - s->roi_first + 1;
+    uint64_t cells = 1;
+    for (int q = 0; q < P; ++q) cells *= (uint64_t)s->c[q].count;
+    const int policy = opt ? opt->trajectory : 0;
+    scan_t sc;
+    memset(&sc, 0, sizeof(sc));
+    sc.retain = opt ? opt->retain_threshold : 0.0;
+    sc.keep_dense = opt ? opt->keep_dense : 0;
+    sc.best_m = -1.0;
+    if (sc.keep_dense) sc.dense = calloc(cells * (uint64_t)R ? cells * (uint64_t)R : 1, sizeof(cplx));
+    cplx *cube = to_cplx(cube_d, (size_t)K * M);
+    const double dop_scale = 4.0 * M_PI / lambda_of(p), bin_scale = 2.0 * p->fs / C_LIGHT;
+    double *offset = malloc(sizeof(double) * M);
+    cplx *phase = malloc(sizeof(cplx) * M);
+    int rc = LTCI_OK;
+    for (uint64_t cidx = 0; cidx < cells && rc == LTCI_OK; ++cidx) {
+        /* decode_motion (proj/src/detectors.cpp:84-92): c_1 fastest */
+        double cv[LTCI_MAX_ORDER];
+        uint64_t rem = cidx;
+        for (int q = 0; q < P; ++q) {
+            int ip = (int)(rem % (uint64_t)s->c[q].count);
+            rem /= (uint64_t)s->c[q].count;
+            cv[q] = s->c[q].start + s->c[q].step * ip;
+        }
+        for (int m = 0; m < M; ++m) {
+            double sv = poly_from(cv, P, slow_time(p, m), 1);
+            offset[m] = bin_scale * sv;
+            phase[m] = polar1(dop_scale * sv);
+        }
+        for (int r = 0; r < R && rc == LTCI_OK; ++r) {
+            int n0 = s->roi_first + r;
+            cplx acc = 0;
+            for (int m = 0; m < M; ++m) {
+                long n = lround((double)n0 + offset[m]);
+                if (n < 0 || n >= K) {
+                    if (policy == 0) continue;
+                    if (policy == 1) {
+                        n = ((n % K) + K) % K;
+                    } else {
+                        rc = LTCI_OUT_OF_RANGE;
+                        break;
+                    }
+                }
+                acc += cube[n + (size_t)K * m] * phase[m];
+            }
+            if (rc == LTCI_OK) scan_consider(&sc, cidx * (uint64_t)R + (uint64_t)r, acc);
+        }
+    }
+    free(offset);
+    free(phase);
+    free(cube);
+    if (rc != LTCI_OK) {
+        free(sc.cand);
+        free(sc.dense);
+        return rc;
+    }
+    ltci_detection_map *mp = calloc(1, sizeof(*mp));
+    mp->kind = LTCI_TD_GRFT;
+    int a = 0; /* single_scale_axes (proj/src/detectors.cpp:94-101) */
+    for (int q = P; q >= 2; --q) mp->axes[a++] = (ltci_axis){LTCI_AXIS_HIGHER, q, s->c[q - 1].count};
+    mp->axes[a++] = (ltci_axis){LTCI_AXIS_VELOCITY, 1, s->c[0].count};
+    mp->axes[a++] = (ltci_axis){LTCI_AXIS_RANGE, 0, R};
+    mp->n_axes = a;
+    mp->counters[1] = cells * (uint64_t)R;
+    scan_finish(&sc, mp, cells * (uint64_t)R);
+    *out = mp;
+    return LTCI_OK;
+}
+
+/* kt_mfp (proj/src/detectors.cpp:266-326): keystone once; per (q, c2) cell
+ * gift(KtRm) -- y .* H_KtRm, dft_plus(K) per pulse, no preDFM -- then gft({c2}). */
+int oracle_kt_mfp(const double *cube_d, const ltci_radar *p, const ltci_ambiguity *amb, const ltci_single_space *s,
+                  const ltci_options *opt, ltci_detection_map **out) {
+    const int K = p->K, M = p->M;
+    if (!same_radar(p, &s->radar) || s->order != 2) return LTCI_INVALID_ARGUMENT;
+    const int R = s->roi_last - s->roi_first + 1;
+    if (R <= 0 || s->roi_first < 0 || s->roi_last >= K) return LTCI_INVALID_ARGUMENT;
+    const int nq = amb->q_max - amb->q_min + 1, n2 = s->c[1].count;
+    const uint64_t cells = (uint64_t)nq * (uint64_t)n2, total = cells * (uint64_t)R * (uint64_t)M;
+    scan_t sc;
+    memset(&sc, 0, sizeof(sc));
+    sc.retain = opt ? opt->retain_threshold : 0.0;
+    sc.keep_dense = opt ? opt->keep_dense : 0;
+    sc.best_m = -1.0;
+    if (sc.keep_dense) sc.dense = calloc(total ? total : 1, sizeof(cplx));
+    cplx *cube = to_cplx(cube_d, (size_t)K * M), *kt = malloc(sizeof(cplx) * (size_t)K * M);
+    keystone_impl(cube, p, opt && opt->keystone_taps > 0 ? opt->keystone_taps : 8, kt);
+    cplx *comp = malloc(sizeof(cplx) * (size_t)K * M), *h = malloc(sizeof(cplx) * M);
+    cplx *y = malloc(sizeof(cplx) * M), *scratch = malloc(sizeof(cplx) * 2 * M);
+    cplx *twK = twiddles(K), *twM = twiddles(M);
+    const double s4 = 4.0 * M_PI / C_LIGHT;
+    for (uint64_t cidx = 0; cidx < cells; ++cidx) {
+        const int i2 = (int)(cidx % (uint64_t)n2), iq = (int)(cidx / (uint64_t)n2);
+        const double c2 = s->c[1].start + s->c[1].step * i2, qva = (double)(amb->q_min + iq) * va_of(p);
+        for (int m = 0; m < M; ++m) { /* build_mf(KtRm) + compensated_ifft (transforms.cpp:53-70,134-147) */
+            const double tm = slow_time(p, m);
+            cplx *dst = comp + (size_t)K * m;
+            const cplx *src = kt + (size_t)K * m;
+            for (int k = 0; k < K; ++k) {
+                double fk = freq_of_row(p, k), fbar = 1.0 - fk / p->fc;
+                dst[k] = src[k] * polar1(s4 * fk * (fbar * qva * tm - c2 * tm * tm));
+            }
+            fft_plus(dst, K, twK);
+        }
+        dfm_chirp(p, &c2, 1, h);
+        const uint64_t base = cidx * (uint64_t)R * (uint64_t)M;
+        for (int r = 0; r < R; ++r) {
+            gft_row(comp, p, s->roi_first + r, h, y, scratch, twM);
+            for (int j = 0; j < M; ++j) scan_consider(&sc, base + (uint64_t)r * M + (uint64_t)j, y[j]);
+        }
+    }
+    free(cube);
+    free(kt);
+    free(comp);
+    free(h);
+    free(y);
+    free(scratch);
+    free(twK);
+    free(twM);
+    ltci_detection_map *mp = calloc(1, sizeof(*mp));
+    mp->kind = LTCI_KT_MFP;
+    mp->axes[0] = (ltci_axis){LTCI_AXIS_FOLDING, 0, nq};
+    mp->axes[1] = (ltci_axis){LTCI_AXIS_HIGHER, 2, n2};
+    mp->axes[2] = (ltci_axis){LTCI_AXIS_RANGE, 0, R};
+    mp->axes[3] = (ltci_axis){LTCI_AXIS_DOPPLER, 0, M};
+    mp->n_axes = 4;
+    mp->counters[0] = 1;
+    mp->counters[1] = cells * (uint64_t)K;
+    mp->counters[2] = cells * (uint64_t)M;
+    mp->counters[3] = cells * (uint64_t)R;
+    scan_finish(&sc, mp, total);
+    *out = mp;
     return LTCI_OK;
 }

@@ -51,6 +51,8 @@ int guarded(F&& f) {
         return fail(LTCI_IO_ERROR, e.what());
     } catch (const std::invalid_argument& e) {
         return fail(LTCI_INVALID_ARGUMENT, e.what());
+    } catch (const std::out_of_range& e) {
+        return fail(LTCI_OUT_OF_RANGE, e.what());
     } catch (const std::bad_alloc& e) {
         return fail(LTCI_BAD_ALLOC, e.what());
     } catch (const std::exception& e) {
@@ -159,6 +161,7 @@ R::DetectorOptions options_of(const ltci_options* o) {
         opt.keep_dense = o->keep_dense != 0;
         opt.threads = o->threads;
         opt.keystone_taps = o->keystone_taps > 0 ? o->keystone_taps : 8;
+        opt.trajectory = static_cast<R::TrajectoryPolicy>(o->trajectory);
     }
     return opt;
 }
@@ -562,6 +565,29 @@ int ref_fd_grft(const double* cube, const ltci_radar* r, const ltci_single_space
     return guarded([&] {
         R::FreqPulseCube c = cube_of(cube, radar_of(*r));
         *out = map_to(R::fd_grft(c, single_of(*s), options_of(o)));
+    });
+}
+
+// td_grft (proj/src/detectors.cpp:199-264): range-pulse cube in, std::out_of_range under the Error policy
+int ref_td_grft(const double* cube, const ltci_radar* r, const ltci_single_space* s, const ltci_options* o,
+                ltci_detection_map** out) {
+    return guarded([&] {
+        R::RangePulseCube c(radar_of(*r));
+        const std::size_t n = static_cast<std::size_t>(r->K) * r->M;
+        for (std::size_t i = 0; i < n; ++i) c.data[i] = R::cplx(cube[2 * i], cube[2 * i + 1]);
+        *out = map_to(R::td_grft(c, single_of(*s), options_of(o)));
+    });
+}
+
+// kt_mfp (proj/src/detectors.cpp:266-326)
+int ref_kt_mfp(const double* cube, const ltci_radar* r, const ltci_ambiguity* a, const ltci_single_space* s,
+               const ltci_options* o, ltci_detection_map** out) {
+    return guarded([&] {
+        R::FreqPulseCube c = cube_of(cube, radar_of(*r));
+        R::AmbiguitySpace amb;
+        amb.q_min = a->q_min;
+        amb.q_max = a->q_max;
+        *out = map_to(R::kt_mfp(c, amb, single_of(*s), options_of(o)));
     });
 }
 

@@ -10,7 +10,7 @@ import ctypes as C
 MAX_ORDER = 4
 MAX_AXES = 12
 
-OK, INVALID_ARGUMENT, CONDITION_VIOLATED, RUNTIME_ERROR, BAD_ALLOC, NO_DEVICE, IO_ERROR = range(7)
+OK, INVALID_ARGUMENT, CONDITION_VIOLATED, RUNTIME_ERROR, BAD_ALLOC, NO_DEVICE, IO_ERROR, OUT_OF_RANGE = range(8)
 FD_GRFT, TD_GRFT, KT_MFP, DS_GRFT, DS_KT_MFP = range(5)
 AXIS_RANGE, AXIS_VELOCITY, AXIS_HIGHER, AXIS_DOPPLER, AXIS_COARSE, AXIS_FINE, AXIS_FOLDING = range(7)
 VARIANT_GRFT, VARIANT_KTMFP = 0, 1

@@ -21,7 +21,7 @@ EXPORTS = (
     "ltci_cuda_mgift", "ltci_cuda_gft", "ltci_cuda_detection_threshold", "ltci_engine_create",
     "ltci_engine_destroy", "ltci_engine_run_device", "ltci_engine_run_host", "ltci_engine_result",
     "ltci_engine_peaks_device", "ltci_engine_stats", "ltci_engine_set_timing", "ltci_engine_fine_path", "ltci_engine_coarse_path",
-    "ltci_engine_work", "ltci_engine_run_file", "ltci_engine_set_coarse_slice", "ltci_cuda_merge_peaks", "ltci_cuda_fd_grft", "ltci_cuda_extract_detections_single",
+    "ltci_engine_work", "ltci_engine_run_file", "ltci_engine_set_coarse_slice", "ltci_cuda_merge_peaks", "ltci_cuda_fd_grft", "ltci_cuda_td_grft", "ltci_cuda_kt_mfp", "ltci_cuda_extract_detections_single",
     "ltci_cuda_extract_detections", "ltci_cuda_cube_file_info", "ltci_cuda_cube_file_read",
     "ltci_cuda_cube_file_write", "ltci_cuda_synthesize", "ltci_cuda_add_noise", "ltci_cuda_run_pd", "ltci_cuda_measure_fp32_peak", "ltci_cuda_pool_idle", "ltci_cuda_last_error", "ltci_cuda_version",
 )
@@ -53,6 +53,8 @@ def raise_for(rc: int, lib) -> None:
         raise MemoryError(msg)  # std::bad_alloc
     if rc == A.IO_ERROR:
         raise IoError(msg)
+    if rc == A.OUT_OF_RANGE:
+        raise IndexError(msg)  # std::out_of_range
     raise LtciError(msg)
 
 
@@ -123,6 +125,8 @@ def load():
     lib.ltci_cuda_add_noise.argtypes = [vp, P(A.CRadar), C.c_double, C.c_uint64, vp]
     lib.ltci_cuda_run_pd.argtypes = [P(A.CScenario), P(A.CPdPoint)]
     lib.ltci_cuda_fd_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
+    lib.ltci_cuda_td_grft.argtypes = [vp, P(A.CRadar), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
+    lib.ltci_cuda_kt_mfp.argtypes = [vp, P(A.CRadar), P(A.CAmbiguity), P(A.CSingleSpace), P(A.COptions), P(A.PMap)]
     lib.ltci_cuda_extract_detections_single.argtypes = [P(A.CDetectionMap), P(A.CSingleSpace), C.c_double,
                                                         P(A.CDetection), C.c_int, P(C.c_int)]
     lib.ltci_cuda_last_error.restype = C.c_char_p

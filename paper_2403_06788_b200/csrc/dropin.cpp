@@ -1,4 +1,5 @@
-// dropin.cpp -- ltci::ds_grft / ltci::ds_kt_mfp / ltci::fd_grft on the B200 (libltci_b200.so).
+// dropin.cpp -- ltci::ds_grft / ltci::ds_kt_mfp / ltci::fd_grft / ltci::td_grft / ltci::kt_mfp on the
+// B200 (libltci_b200.so): the five detectors of proj/include/ltci/detectors.hpp.
 //
 // Same signatures, argument meaning and exceptions as the reference
 // (proj/include/ltci/detectors.hpp:42-48, proj/src/detectors.cpp:414-481):
@@ -86,6 +87,7 @@ ltci_options to_c(const ltci::DetectorOptions& o) {
         case LTCI_INVALID_ARGUMENT: throw std::invalid_argument(msg);
         case LTCI_CONDITION_VIOLATED: throw ltci::ConditionViolated(msg);
         case LTCI_BAD_ALLOC: throw std::bad_alloc();
+        case LTCI_OUT_OF_RANGE: throw std::out_of_range(msg);
         default: throw std::runtime_error(msg);
     }
 }
@@ -141,6 +143,40 @@ DetectionMap fd_grft(const FreqPulseCube& cube, const SingleScaleSpace& space, c
     if (rc != LTCI_OK) rethrow(rc);
     DetectionMap m = to_cpp(*g.m, cube.params);
     m.single = space;
+    return m;
+}
+
+// proj/src/detectors.cpp:199-264
+DetectionMap td_grft(const RangePulseCube& cube, const SingleScaleSpace& space, const DetectorOptions& opt) {
+    const ltci_radar r = to_c(cube.params);
+    const ltci_single_space s = to_c(space);
+    const ltci_options o = to_c(opt);
+    MapGuard g;
+    const std::size_t n = static_cast<std::size_t>(cube.params.K) * cube.params.M;
+    if (cube.data.size() != n) throw std::invalid_argument("detector: cube data size does not match K*M");
+    const int rc = ltci_cuda_td_grft(reinterpret_cast<const double*>(cube.data.data()), &r, &s, &o, &g.m);
+    if (rc != LTCI_OK) rethrow(rc);
+    DetectionMap m = to_cpp(*g.m, cube.params);
+    m.single = space;
+    return m;
+}
+
+// proj/src/detectors.cpp:266-326
+DetectionMap kt_mfp(const FreqPulseCube& cube, const AmbiguitySpace& amb, const SingleScaleSpace& space,
+                    const DetectorOptions& opt) {
+    const ltci_radar r = to_c(cube.params);
+    if (space.c.size() != 2) throw std::invalid_argument("kt_mfp: needs a P = 2 search space");
+    const ltci_single_space s = to_c(space);
+    const ltci_options o = to_c(opt);
+    const ltci_ambiguity a{amb.q_min, amb.q_max};
+    MapGuard g;
+    const std::size_t n = static_cast<std::size_t>(cube.params.K) * cube.params.M;
+    if (cube.data.size() != n) throw std::invalid_argument("detector: cube data size does not match K*M");
+    const int rc = ltci_cuda_kt_mfp(reinterpret_cast<const double*>(cube.data.data()), &r, &a, &s, &o, &g.m);
+    if (rc != LTCI_OK) rethrow(rc);
+    DetectionMap m = to_cpp(*g.m, cube.params);
+    m.single = space;
+    m.amb = amb;
     return m;
 }
 

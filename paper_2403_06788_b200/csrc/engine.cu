@@ -33,6 +33,7 @@
 #include "fine_fft.cuh"
 #include "fine_tc.cuh"
 #include "fd_grft.cuh"
+#include "td_grft.cuh"
 #include "range_fft.cuh"
 #include "fine_launch.hpp"
 #include "gather_launch.hpp"
@@ -1556,8 +1557,10 @@ struct FdWorkspace {
     DevBuf<float2> v0, v1;
     DevBuf<double2> vo;
     DevBuf<unsigned char> tmp;
+    DevBuf<int> err;
     HostBuf<unsigned char> small;
     HostBuf<float2> dense_h;
+    HostBuf<int> err_h;
     Stager stager;
 };
 
@@ -1566,22 +1569,29 @@ ObjectPool<FdWorkspace>& fd_pool() {
     return *p;
 }
 
-ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const ltci_radar& rp,
-                                const ltci_single_space& s, const ltci_options* opt) {
+// The single-scale searches fd_grft (frequency-pulse cube; K5 + K6) and td_grft
+// (range-pulse cube; K7, proj/src/detectors.cpp:199-264) share everything but
+// the kernels: the motion grid and its cell index, the ROI scan, the result.
+ltci_detection_map* single_scale_run(int kind, const double* cube, const float2* d_cube, const ltci_radar& rp,
+                                     const ltci_single_space& s, const ltci_options* opt) {
+    const bool td = kind == LTCI_TD_GRFT;
+    const std::string who = td ? "td_grft" : "fd_grft";
     validate_radar(rp);
     check_same_params(rp, s.radar);
     if (rp.K < 2 || rp.K > 8192) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: frequency bins K must be in [2, 8192]");
-    if (rp.M > 1 << 20) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: fd_grft supports M <= 2^20");
+    if (rp.M > 1 << 20) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: " + who + " supports M <= 2^20");
     const int P = s.order;
-    if (P < 1 || P > LTCI_MAX_ORDER) fail(LTCI_INVALID_ARGUMENT, "fd_grft: order must be in [1, 4]");
+    if (P < 1 || P > LTCI_MAX_ORDER) fail(LTCI_INVALID_ARGUMENT, who + ": order must be in [1, 4]");
     unsigned long long cells = 1;
     for (int p = 0; p < P; ++p) {
         if (s.c[p].count < 1) fail(LTCI_INVALID_ARGUMENT, "grid is empty");
         cells *= static_cast<unsigned long long>(s.c[p].count);
     }
     if (s.roi_first < 0 || s.roi_last >= rp.K || s.roi_first > s.roi_last)
-        fail(LTCI_INVALID_ARGUMENT, "fd_grft: ROI outside the range axis");
+        fail(LTCI_INVALID_ARGUMENT, who + ": ROI outside the range axis");
     const int R = s.roi_last - s.roi_first + 1;
+    const int policy = opt ? opt->trajectory : 0;
+    if (td && (policy < 0 || policy > 2)) fail(LTCI_INVALID_ARGUMENT, "td_grft: unknown trajectory policy");
     const int device = opt ? opt->device : 0;
     const double retain = opt ? opt->retain_threshold : 0.0;
     const bool keep_dense = opt && opt->keep_dense;
@@ -1622,7 +1632,7 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
         if (bytes > static_cast<double>(256u << 20)) {  // the (slow) memory query only for big maps
             CK(cudaMemGetInfo(&free_b, &total_b));
             if (bytes > 0.5 * static_cast<double>(free_b) || bytes * 2 > 64.0 * (1ull << 30))
-                fail(LTCI_BAD_ALLOC, "ltci_cuda: dense fd_grft map exceeds the result memory");
+                fail(LTCI_BAD_ALLOC, "ltci_cuda: dense " + who + " map exceeds the result memory");
         }
         dense.ensure(static_cast<size_t>(cells) * R);
     }
@@ -1630,9 +1640,14 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
     const unsigned long long gran = std::max<unsigned long long>(kFdCells, kCoarseSamples / K);
     unsigned long long batch = std::max<unsigned long long>(gran, ((2ull << 30) / (8ull * K)) / gran * gran);
     batch = std::min(batch, (cells + gran - 1) / gran * gran);
-    acc.ensure(static_cast<size_t>(batch) * K);
+    if (td)
+        batch = std::min<unsigned long long>(cells, 1u << 30);  // one CTA column per cell: the grid's x extent
+    else
+        acc.ensure(static_cast<size_t>(batch) * K);
     ccount.ensure(1);
     best.ensure(1);
+    w.err.ensure(1);
+    w.err_h.ensure(1);
 
     FdArgs a{};
     a.cube = d_cube ? d_cube : c64.p;
@@ -1648,6 +1663,9 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
     a.inv_prf = 1.0 / rp.PRF;
     a.two_over_lambda = 2.0 / lambda_of(rp);
     a.two_df_over_c = 2.0 * rp.delta_f / kC;
+    a.bin_scale = 2.0 * rp.fs / kC;  // metres -> range bins (detectors.cpp:220)
+    a.policy = policy;
+    a.err = w.err.p;
     a.roi_first = s.roi_first;
     a.R = R;
     a.retain2 = retain < 0 ? -1.0f : static_cast<float>(retain * retain);
@@ -1665,11 +1683,19 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
         CK(cudaMemsetAsync(ccount.p, 0, sizeof(unsigned long long), st));
         init_slots_kernel<<<1, 32, 0, st>>>(best.p, 1);
         CK(cudaGetLastError());
+        if (td) CK(cudaMemsetAsync(w.err.p, 0, sizeof(int), st));
         for (unsigned long long c0 = 0; c0 < cells; c0 += batch) {
             a.c_begin = c0;
             a.c_count = std::min(batch, cells - c0);
-            fd_launch(a, st);
+            if (td) {
+                td_gather_scan_kernel<<<dim3(static_cast<unsigned>(a.c_count), (R + kTdThreads - 1) / kTdThreads),
+                                        kTdThreads, 0, st>>>(a);
+                CK(cudaGetLastError());
+            } else {
+                fd_launch(a, st);
+            }
         }
+        if (td) CK(cudaMemcpyAsync(w.err_h.p, w.err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         // count, best cell and small candidate sets behind one synchronisation
         hb = enqueue_small_result(w.small, ccount.p, cand.p, cap, best.p, 1, 1, M / 2, M, st);
         if (nd) {
@@ -1677,6 +1703,7 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
             CK(cudaMemcpyAsync(w.dense_h.p, dense.p, nd * sizeof(float2), cudaMemcpyDeviceToHost, st));
         }
         CK(cudaStreamSynchronize(st));
+        if (td && *w.err_h.p) fail(LTCI_OUT_OF_RANGE, "td_grft: trajectory leaves the cube");
         count = *reinterpret_cast<volatile unsigned long long*>(hb);
         if (count <= cap) break;
         CK(cudaMemGetInfo(&free_b, &total_b));
@@ -1690,15 +1717,19 @@ ltci_detection_map* fd_grft_run(const double* cube, const float2* d_cube, const 
     auto* out = static_cast<ltci_detection_map*>(std::calloc(1, sizeof(ltci_detection_map)));
     if (!out) throw std::bad_alloc();
     try {
-        out->kind = LTCI_FD_GRFT;
+        out->kind = kind;
         // single_scale_axes (detectors.cpp:94-101): c_P .. c_2, c_1, range
         int na = 0;
         for (int p = P; p >= 2; --p) out->axes[na++] = ltci_axis{LTCI_AXIS_HIGHER, p, s.c[p - 1].count};
         out->axes[na++] = ltci_axis{LTCI_AXIS_VELOCITY, 1, s.c[0].count};
         out->axes[na++] = ltci_axis{LTCI_AXIS_RANGE, 0, R};
         out->n_axes = na;
-        out->counters[1] = cells * static_cast<unsigned long long>(K);  // mf += n0() per cell
-        out->counters[2] = cells;                                       // ifft += 1 per cell
+        if (td) {
+            out->counters[1] = cells * static_cast<unsigned long long>(R);  // mf += 1 per (cell, row)
+        } else {
+            out->counters[1] = cells * static_cast<unsigned long long>(K);  // mf += n0() per cell
+            out->counters[2] = cells;                                       // ifft += 1 per cell
+        }
         out->retain_threshold = retain;
         const PeakSlot b = *reinterpret_cast<const PeakSlot*>(hb + L.slots);
         out->argmax = b.idx;
@@ -1759,7 +1790,7 @@ __global__ void merge_peaks_kernel(const PeakSlot* __restrict__ in, int n_maps, 
 ltci_detection_map* ltcib_fd_grft_device(const float2* d_cube, const ltci_radar& rp, const ltci_single_space& s,
                                          const ltci_options* opt) {
     try {
-        return fd_grft_run(nullptr, d_cube, rp, s, opt);
+        return single_scale_run(LTCI_FD_GRFT, nullptr, d_cube, rp, s, opt);
     } catch (const Error& e) {
         throw ltcib::CubeError(e.code, e.msg);  // status-carrying error across translation units
     }
@@ -1811,7 +1842,61 @@ int ltci_cuda_fd_grft(const double* cube, const ltci_radar* cube_params, const l
                       const ltci_options* opt, ltci_detection_map** out) {
     return guarded([&] {
         if (!cube || !cube_params || !space || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
-        *out = fd_grft_run(cube, nullptr, *cube_params, *space, opt);
+        *out = single_scale_run(LTCI_FD_GRFT, cube, nullptr, *cube_params, *space, opt);
+    });
+}
+
+int ltci_cuda_td_grft(const double* cube, const ltci_radar* cube_params, const ltci_single_space* space,
+                      const ltci_options* opt, ltci_detection_map** out) {
+    return guarded([&] {
+        if (!cube || !cube_params || !space || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        *out = single_scale_run(LTCI_TD_GRFT, cube, nullptr, *cube_params, *space, opt);
+    });
+}
+
+// kt_mfp (proj/src/detectors.cpp:266-326) is the dual-scale keystone cascade
+// with one fine cell: per (folding number, acceleration) cell gift(KtRm) then
+// gft({c2}) -- the preDFM factor of mgift carries the whole c2 t^2 phase when
+// the fine offset is zero -- over the full Doppler axis; the flat index
+// ((q, c2), r, j) is ds_kt_mfp's with a fine axis of size one.
+int ltci_cuda_kt_mfp(const double* cube, const ltci_radar* cube_params, const ltci_ambiguity* amb,
+                     const ltci_single_space* space, const ltci_options* opt, ltci_detection_map** out) {
+    return guarded([&] {
+        if (!cube || !cube_params || !amb || !space || !out) fail(LTCI_INVALID_ARGUMENT, "ltci_cuda: null argument");
+        check_same_params(*cube_params, space->radar);
+        if (space->order != 2) fail(LTCI_INVALID_ARGUMENT, "kt_mfp: needs a P = 2 search space");
+        ltci_dual_space d{};
+        d.radar = space->radar;
+        d.order = 2;
+        d.coarse[0] = ltci_grid{0.0, 1.0, 1};  // unused by the keystone variant
+        d.coarse[1] = space->c[1];
+        d.fine[0] = ltci_grid{0.0, 1.0, 1};
+        d.fine[1] = ltci_grid{0.0, 1.0, 1};    // the single fine cell: zero offset
+        for (int p = 0; p < 2; ++p) {
+            d.rm_step[p] = space->rm_step[p];
+            d.dfm_step[p] = space->dfm_step[p];
+            d.alpha[p] = space->alpha[p];
+        }
+        d.kappa = 1.0;
+        d.roi_first = space->roi_first;
+        d.roi_last = space->roi_last;
+        ltci_detection_map* m = nullptr;
+        const int rc = detect(cube, cube_params, amb, &d, opt, LTCI_VARIANT_KTMFP, &m);
+        if (rc != LTCI_OK) throw Error{rc, g_err};
+        const unsigned long long cells =
+            static_cast<unsigned long long>(amb->q_max - amb->q_min + 1) * static_cast<unsigned long long>(space->c[1].count);
+        const int R = space->roi_last - space->roi_first + 1;
+        m->kind = LTCI_KT_MFP;
+        m->n_axes = 4;
+        m->axes[0] = ltci_axis{LTCI_AXIS_FOLDING, 0, amb->q_max - amb->q_min + 1};
+        m->axes[1] = ltci_axis{LTCI_AXIS_HIGHER, 2, space->c[1].count};
+        m->axes[2] = ltci_axis{LTCI_AXIS_RANGE, 0, R};
+        m->axes[3] = ltci_axis{LTCI_AXIS_DOPPLER, 0, cube_params->M};
+        m->counters[0] = 1;                                                      // kt
+        m->counters[1] = cells * static_cast<unsigned long long>(cube_params->K);  // mf += n0() per cell
+        m->counters[2] = cells * static_cast<unsigned long long>(cube_params->M);  // ifft += M per cell
+        m->counters[3] = cells * static_cast<unsigned long long>(R);               // fft += R per cell
+        *out = m;
     });
 }
 

@@ -37,6 +37,11 @@ struct FdArgs {
     int count[4];                 // grid counts, order p at [p-1] (c_1 fastest in the cell index)
     double start[4], step[4];
     double inv_prf, two_over_lambda, two_df_over_c;
+    // td_grft (td_grft.cuh): metres -> range bins, TrajectoryPolicy (0 zero outside, 1 wrap, 2 error)
+    // and the flag the error policy raises
+    double bin_scale;
+    int policy;
+    int* err;
     // scan
     int roi_first, R;
     float retain2;                // retain^2 (-1: retain everything)

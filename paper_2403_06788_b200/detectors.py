@@ -79,6 +79,41 @@ def fd_grft(cube: np.ndarray, params: RadarParams, space: SingleScaleSpace,
     return m
 
 
+def td_grft(range_cube: np.ndarray, params: RadarParams, space: SingleScaleSpace,
+            opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    """Single-scale time-domain GRFT on the GPU (ltci::td_grft,
+    proj/src/detectors.cpp:199-264): nearest-bin sums along rounded
+    trajectories of a RANGE-pulse cube.  ``opt.trajectory``: 0 zero outside,
+    1 wrap, 2 raise IndexError (std::out_of_range) when a trajectory leaves
+    the cube."""
+    lib = _lib.load()
+    opt = opt or DetectorOptions()
+    data = cube_as_f64(range_cube, params)
+    r, s, o = params.to_c(), space.to_c(), opt.to_c()
+    pm = A.PMap()
+    _lib.raise_for(lib.ltci_cuda_td_grft(_f64_ptr(data), C.byref(r), C.byref(s), C.byref(o), C.byref(pm)), lib)
+    m = _take_map(lib, pm, params)
+    m.single = space
+    return m
+
+
+def kt_mfp(cube: np.ndarray, params: RadarParams, amb: AmbiguitySpace, space: SingleScaleSpace,
+           opt: Optional[DetectorOptions] = None) -> DetectionMap:
+    """Single-scale keystone matched-filter processing on the GPU (ltci::kt_mfp,
+    proj/src/detectors.cpp:266-326): keystone once, then (folding number,
+    acceleration) cells over the full Doppler axis; ``space`` must have order 2."""
+    lib = _lib.load()
+    opt = opt or DetectorOptions()
+    data = cube_as_f64(cube, params)
+    r, s, o, a = params.to_c(), space.to_c(), opt.to_c(), amb.to_c()
+    pm = A.PMap()
+    _lib.raise_for(lib.ltci_cuda_kt_mfp(_f64_ptr(data), C.byref(r), C.byref(a), C.byref(s), C.byref(o),
+                                        C.byref(pm)), lib)
+    m = _take_map(lib, pm, params)
+    m.single, m.amb = space, amb
+    return m
+
+
 def detection_threshold(params: RadarParams, sigma2: float, pfa: float, bins: int = 0) -> float:
     lib = _lib.load()
     st = C.c_int(0)

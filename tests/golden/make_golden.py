@@ -20,11 +20,14 @@ what the reference's own functions return:
   fd.npz           fd_grft at orders 1, 2 and 3 on
                    build_single_scale spaces, keep_dense + candidates; the order-2
                    case with a sub-ROI
+  td_kt.npz        td_grft on a range-pulse cube (orders 1 and 2, ROI subset, the
+                   ZeroOutside and Wrap trajectory policies) and kt_mfp (three
+                   folding numbers), keep_dense + candidates
   range_fft.npz    range_fft (the configs[3] front end K0) of seeded range-pulse
                    cubes: a noise cube, and range_ifft of a synthesized
                    DS-KT-MFP scene (K_valid < K guard band) with its round trip
 
-    python tests/golden/make_golden.py [fd|range]     (fd / range: only that file)
+    python tests/golden/make_golden.py [fd|td_kt|range]     (only that file)
 """
 from __future__ import annotations
 
@@ -92,6 +95,37 @@ def make_fd():
     np.savez_compressed(os.path.join(HERE, "fd.npz"), **out)
 
 
+def make_td_kt():
+    """td_grft (range-pulse cube, the three trajectory policies) and kt_mfp from the reference."""
+    p = O.ref_radar(8 * 100e6, 100e6, 50e6, 2000.0, 32, 64)
+    tgt = [(0.4 + 0.1j, [21 * p.delta_R(), 13.3, 240.0]), (0.3, [40 * p.delta_R(), -22.0, -400.0])]
+    freq = c64(O.ref_synthesize(p, tgt, 1.0 / p.K, 92))
+    rng_cube = c64(O.ref_range_ifft(freq, p))
+    out = {"freq": freq.astype(np.complex64), "range": rng_cube.astype(np.complex64), **radar_arrays("", p)}
+    # td_grft: order 2 with an ROI subset (trajectories leave the cube at both ends) and order 1
+    s2 = O.ref_single_scale(p, 2, [(-30.0, 30.0), (-1100.0, 1100.0)], [0.5, 0.5], 2, p.K - 3)
+    s1 = O.ref_single_scale(p, 1, [(-30.0, 30.0)], [1.0], 0, p.K - 1)
+    probe = O.ref_td(rng_cube, p, s2, DetectorOptions(keep_dense=True))
+    retain = float(np.quantile(np.abs(probe.dense), 0.8))
+    out["td_retain"] = np.array(retain)
+    out.update(single_arrays("s2_", s2), **single_arrays("s1_", s1))
+    for pol, name in ((0, "zero"), (1, "wrap")):
+        opt = DetectorOptions(retain_threshold=retain, keep_dense=True, trajectory=pol)
+        out.update(map_arrays(f"td2_{name}_", O.ref_td(rng_cube, p, s2, opt)))
+    out.update(map_arrays("td1_zero_", O.ref_td(rng_cube, p, s1, DetectorOptions(retain_threshold=retain,
+                                                                                   keep_dense=True))))
+    # kt_mfp: three folding numbers, acceleration grid of the order-2 space
+    amb = O.ref_ambiguity(p, -1.4 * p.Va(), 1.4 * p.Va())
+    sk = O.ref_single_scale(p, 2, [(-30.0, 30.0), (-1100.0, 1100.0)], [0.5, 0.5], 4, p.K - 9)
+    probe = O.ref_kt(freq, p, amb, sk, DetectorOptions(keep_dense=True))
+    kret = float(np.quantile(np.abs(probe.dense), 0.9))
+    out["kt_retain"] = np.array(kret)
+    out["amb"] = np.array([amb.q_min, amb.q_max])
+    out.update(single_arrays("sk_", sk),
+               **map_arrays("kt_", O.ref_kt(freq, p, amb, sk, DetectorOptions(retain_threshold=kret, keep_dense=True))))
+    np.savez_compressed(os.path.join(HERE, "td_kt.npz"), **out)
+
+
 def make_range():
     # noise cube straight in the range domain, and a C3-like scene (fs > Br) taken
     # to the range domain by the reference's range_ifft
@@ -110,6 +144,10 @@ def main():
     if sys.argv[1:] == ["fd"]:
         make_fd()
         print("fd.npz written to", HERE)
+        return
+    if sys.argv[1:] == ["td_kt"]:
+        make_td_kt()
+        print("td_kt.npz written to", HERE)
         return
     if sys.argv[1:] == ["range"]:
         make_range()
@@ -166,6 +204,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "c0.npz"), cube=cube.astype(np.complex64), gamma=np.array(gamma),
                         peak_index=pi, peak_value=pv, **map_arrays("", m))
     make_fd()
+    make_td_kt()
     make_range()
     print("golden vectors written to", HERE)
 

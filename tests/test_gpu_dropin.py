@@ -26,6 +26,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_dropin")
 BIN_FD = os.path.join(ROOT, "oracle", "_ref", "acceptance_dropin_fd")
+BIN_KT = os.path.join(ROOT, "oracle", "_ref", "acceptance_dropin_kt")
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not os.path.exists(BIN), reason="drop-in acceptance binary not built")]
@@ -54,6 +55,22 @@ def test_reference_acceptance_through_dropin(criterion):
 def test_reference_acceptance_fd_through_dropin(criterion):
     env = dict(os.environ, LTCI_THREADS=str(os.cpu_count() or 1))
     r = subprocess.run([BIN_FD, str(criterion)], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert f"PASS  criterion {criterion:2d}" in r.stdout
+
+
+@pytest.mark.skipif(not os.path.exists(BIN_KT), reason="kt drop-in acceptance binary not built")
+@pytest.mark.parametrize("criterion", [4, 9])
+def test_reference_acceptance_kt_through_dropin(criterion):
+    """acceptance_dropin_kt also routes ltci::kt_mfp to the GPU: criterion 4
+    (DS-KT-MFP against the full single-scale kt_mfp map on 100 random targets,
+    both on the GPU now) and criterion 9 (the full-scale three-target scene,
+    whose KT-MFP leg runs kt_mfp) pass.  Criterion 1 checks kt_mfp against
+    literal sums at 1e-9 (FP64 definitional equality, outside the FP32
+    contract) and stays with the reference's kt_mfp in acceptance_dropin."""
+    env = dict(os.environ, LTCI_THREADS=str(os.cpu_count() or 1))
+    r = subprocess.run([BIN_KT, str(criterion)], capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert f"PASS  criterion {criterion:2d}" in r.stdout
