@@ -12,6 +12,6 @@ cp $G/smoke.log $P/${tag}_smoke.log
 cp $G/launches_c1.csv $P/${tag}_launches_c1.csv
 cp $G/launches_c3.csv $P/${tag}_launches_c3.csv
 for c in c0 c1 c3 c4; do cp $G/ncu_${c}_brief.txt $P/${tag}_ncu_$c.txt; done
-for s in fd pd io; do grep '^{' $G/side_$s.log | tail -1 > $P/${tag}_side_$s.json; done
+for s in fd pd io td; do grep '^{' $G/side_$s.log | tail -1 > $P/${tag}_side_$s.json; done
 grep '^{' $G/side_calls.log > $P/${tag}_side_calls.jsonl
 ls -la $P/${tag}_*

@@ -14,6 +14,7 @@ python bench.py --config 2 --coarse-slice 8 --coarse-rest 1 --steps 2 > gpurun_o
 python bench.py --impl reference > gpurun_out/bench_ref_c1.log 2>&1
 python scripts/bench_fd.py > gpurun_out/side_fd.log 2>&1
 python scripts/bench_pd.py > gpurun_out/side_pd.log 2>&1
+python scripts/bench_td.py > gpurun_out/side_td.log 2>&1
 python scripts/bench_io.py > gpurun_out/side_io.log 2>&1
 python scripts/time_calls.py > gpurun_out/side_calls.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv python scripts/profile_step.py --config 1 > gpurun_out/ncu_launch_c1.log 2>&1
