@@ -17,9 +17,10 @@
 // (coalesced; the 16.8 MB cube lives in L2), the sum runs in packed FP32.
 // Measured on the C0 radar's full single-scale grid (82 971 cells x 512 rows x
 // 256 pulses): 12.8 ms = 852 G trajectory samples/s, 6.8 TB/s of 8-byte
-// gathers -- L2-bandwidth-bound (an integer-only bin computation in place of
-// the FP64 llround changed nothing: 13.5 ms); the reference's td_grft on 16
-// host threads: 3.3 G/s (profiles/r02_side_td.json).
+// gathers; the reference's td_grft on 16 host threads: 3.3 G/s
+// (profiles/r02_side_td.json).  Two variants measured and dropped: an
+// integer-only bin computation in place of the FP64 llround (13.5 ms), and 8
+// neighbouring velocity cells per CTA sharing their loads through L1 (20.4 ms).
 // The ROI scan (threshold candidates, dense store, argmax with the lowest
 // flat index on ties, one 128-bit CAS publish per CTA) is fused.
 #pragma once
