@@ -856,8 +856,9 @@ void engine_init(ltci_engine* e) {
     if (const char* env = std::getenv("LTCI_X_BUDGET_MB")) budget = std::strtoull(env, nullptr, 10) << 20;
     const size_t per_coarse = static_cast<size_t>(pl.R_slice) * M * sizeof(float2);
     e->batch = std::max<unsigned long long>(1, std::min<unsigned long long>(pl.coarse_cells, budget / per_coarse));
-    // the fine kernel indexes rows with int
+    // the fine kernel indexes rows with int; the coarse kernels put the batch's cells on grid.y
     e->batch = std::min<unsigned long long>(e->batch, (1ull << 30) / std::max(1, pl.R_slice));
+    e->batch = std::min<unsigned long long>(e->batch, 65535);
     e->use_tc = tc_fine_selected(pl.fine_path, M, pl.D, pl.keep_dense);
     e->tc_terms = tc_terms_for(pl.fine_path);
     if (!e->use_tc && M == 2048) {

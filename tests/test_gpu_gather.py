@@ -214,3 +214,29 @@ def test_gather_batched_weights_bit_identical(monkeypatch):
     assert np.array_equal(got.peak_index, ref.peak_index)
     assert np.array_equal(got.peak_value, ref.peak_value)
     assert np.array_equal(got.cand_index, ref.cand_index) and np.array_equal(got.cand_value, ref.cand_value)
+
+
+def test_more_coarse_cells_than_one_grid_extent(monkeypatch):
+    """70 000 coarse cells over a one-row ROI (X is 256 B per cell, so the X
+    budget alone would put them in one batch): the engine splits at the grid's
+    65 535-cell extent; both coarse formulations agree on the peak and the
+    retained set."""
+    from paper_2403_06788_b200.configs import baseline_space
+    from paper_2403_06788_b200.model import Grid
+    p = RadarParams.create(3e9, 20e6, 20e6, 1000.0, 32, 64)
+    s = baseline_space(p, [(-50.0, 50.0), (-1.0, 1.0)], roi=RangeRoi(20, 20))
+    s.coarse[0] = Grid(-2000.0, 4000.0 / 7000, 7000)
+    s.coarse[1] = Grid(-50.0, 10.0, 10)
+    s.fine[1] = Grid(0.0, 1.0, 1)
+    x = scene.to_complex64_roundtrip(
+        scene.add_noise(scene.synthesize_cube(p, [(0.5, [20 * p.delta_R(), 333.0, 20.0])]), 1.0 / p.K, 5))
+    w = type("W", (), {"params": p, "space": s, "variant": 0, "amb": None})()
+    out = {}
+    for mode in ("transform", "gather"):
+        monkeypatch.setenv("LTCI_COARSE", mode)
+        out[mode] = _run(w, x, 14.0)[1]
+    a, b = out["transform"], out["gather"]
+    assert a.counters == b.counters and a.counters[2] == 70000 * p.M
+    assert a.argmax == b.argmax
+    assert abs(abs(a.argmax_value) - abs(b.argmax_value)) <= 1e-4 * abs(a.argmax_value)
+    check_candidates(b.cand_index, b.cand_value, a.cand_index, a.cand_value, a.retain_threshold)
