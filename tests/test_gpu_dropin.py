@@ -74,3 +74,20 @@ def test_reference_acceptance_kt_through_dropin(criterion):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert f"PASS  criterion {criterion:2d}" in r.stdout
+
+
+def test_cpp_dropin_td_grft_and_kt_mfp(tmp_path):
+    """A C++ caller of ltci::td_grft / ltci::kt_mfp through libltci_b200.so
+    (tests/cpp/dropin_td_kt.cpp): marshalling, the map by value, std::out_of_range
+    under TrajectoryPolicy::Error and std::invalid_argument for a P = 1 kt space,
+    against the same searches through the C-ABI."""
+    import shutil
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    lib = os.path.join(ROOT, "paper_2403_06788_b200", "lib")
+    exe = str(tmp_path / "dropin_td_kt")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"), "-o", exe,
+                    os.path.join(ROOT, "tests", "cpp", "dropin_td_kt.cpp"), "-L" + lib, "-lltci_b200", "-lltci_cuda",
+                    "-Wl,-rpath," + lib], check=True, capture_output=True, text=True, timeout=300)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "dropin td/kt: ok" in r.stdout, r.stdout + r.stderr
