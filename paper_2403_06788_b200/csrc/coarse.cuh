@@ -36,6 +36,7 @@ struct CoarseArgs {
     double inv_prf, inv_dR, two_over_lambda, Va;
     double kt_b;             // -(4 pi / c) * delta_f^2 / fc  (times q Va t)
     const float* deap;       // TAB = 1: per-frequency-row real scale (gather.cuh deapodisation)
+    int pg;                  // pulses per CTA (0: coarse_pg_for; smaller for plans that would not fill the GPU)
     int npass;
     int radix[8];
 };
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), TAB ? 2 : coarse_min_
     constexpr bool SW = coarse_swizzled<K, OUT16>();
     extern __shared__ float2 smem[];
     constexpr int Kp = CLayout<K, SW>::kp;
-    const int PG = coarse_pg_for(K, a.M, OUT16);
+    const int PG = a.pg ? a.pg : coarse_pg_for(K, a.M, OUT16);
     const int lg_pg = __ffs(PG) - 1;
     float2* buf = smem;
     int* s_shift = reinterpret_cast<int*>(smem + PG * Kp);
@@ -381,8 +382,18 @@ __global__ void __launch_bounds__(coarse_threads<OUT16>(), TAB ? 2 : coarse_min_
     coarse_last_pass<K, RL, OUT16, NT, SW>(a, buf, PG, lg_pg, sc, tid);
 }
 
-inline size_t coarse_smem_bytes(int K, int M, int out16 = 1) {
-    const int PG = coarse_pg_for(K, M, out16);
+// fp32 output: fewer pulses per CTA (down to 4 = one 32-byte sector per row) until the grid has
+// at least 3 CTAs per SM -- small plans (configs[0]: 11 coarse cells x 16 pulse groups = 176 CTAs)
+// are latency-bound on one partial wave otherwise
+inline int coarse_pg_launch(int K, int M, int out16, long long cells) {
+    int pg = coarse_pg_for(K, M, out16);
+    if (!out16)
+        while (pg > 4 && (M / pg) * cells < 148 * 3) pg /= 2;
+    return pg;
+}
+
+inline size_t coarse_smem_bytes(int K, int M, int out16 = 1, int pg = 0) {
+    const int PG = pg ? pg : coarse_pg_for(K, M, out16);
     const int kp = (K == 2048 && !out16) ? CLayout<2048, true>::kp : coarse_kp(K);
     return static_cast<size_t>(PG) * kp * sizeof(float2) + static_cast<size_t>(PG) * (4 + 4 + 4 + 4);
 }

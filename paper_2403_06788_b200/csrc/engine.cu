@@ -432,11 +432,14 @@ void preload_module() {
 }
 
 template <int K, int OUT16>
-void launch_coarse_k(const CoarseArgs& a, cudaStream_t st) {
+void launch_coarse_k(const CoarseArgs& a0, cudaStream_t st) {
     auto kern = coarse_rm_kernel<K, OUT16>;
-    const size_t smem = coarse_smem_bytes(K, a.M, OUT16);
+    CoarseArgs a = a0;
+    static const bool fixed_pg = std::getenv("LTCI_COARSE_FIXED_PG") != nullptr;  // A/B
+    a.pg = fixed_pg ? coarse_pg_for(K, a.M, OUT16) : coarse_pg_launch(K, a.M, OUT16, a.c_count);
+    const size_t smem = coarse_smem_bytes(K, a.M, OUT16, a.pg);
     ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(std::max<size_t>(smem, 160 * 1024)));
-    dim3 grid(a.M / coarse_pg_for(K, a.M, OUT16), a.c_count);
+    dim3 grid(a.M / a.pg, a.c_count);
     kern<<<grid, coarse_threads<OUT16>(), smem, st>>>(a);
     CK(cudaGetLastError());
 }

@@ -15,10 +15,11 @@ __global__ void gather_module_anchor_kernel() {}
 template <int K>
 void launch_tables_k(const CoarseArgs& a, cudaStream_t st) {
     auto kern = coarse_rm_kernel<K, 0, 1>;
-    const size_t smem = coarse_smem_bytes(K, a.M, 0);
+    CoarseArgs b = a;
+    b.pg = coarse_pg_launch(K, a.M, 0, a.c_count);
+    const size_t smem = coarse_smem_bytes(K, a.M, 0, b.pg);
     ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
-    const int pg = coarse_pg_for(K, a.M, 0);
-    kern<<<dim3(a.M / pg, a.c_count), coarse_threads<0>(), smem, st>>>(a);
+    kern<<<dim3(a.M / b.pg, a.c_count), coarse_threads<0>(), smem, st>>>(b);
     cuda_check(cudaGetLastError(), "gather table launch");
 }
 
