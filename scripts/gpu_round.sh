@@ -17,6 +17,8 @@ python scripts/bench_pd.py > gpurun_out/side_pd.log 2>&1
 python scripts/bench_td.py > gpurun_out/side_td.log 2>&1
 python scripts/bench_io.py > gpurun_out/side_io.log 2>&1
 python scripts/time_calls.py > gpurun_out/side_calls.log 2>&1
+python scripts/gather_accuracy.py > gpurun_out/gather_accuracy.jsonl 2> gpurun_out/gather_accuracy.err
+bash scripts/gpu_nccl_one_rank.sh > gpurun_out/nccl_one_rank.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv python scripts/profile_step.py --config 1 > gpurun_out/ncu_launch_c1.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python scripts/profile_step.py --config 3 > gpurun_out/ncu_launch_c3.log 2>&1
 for spec in "c1:1:fine_fft_tm|gather_interp|coarse_rm:3" "c3:3:range_fft|keystone_tiled|fine_fft_tm|coarse:4" "c0:0:fine_fft_tm:1" "c4:4:fine_fft_tm|gather_interp:2"; do
